@@ -1,0 +1,139 @@
+/* drk.h — C ABI of the B200 distributed-ranges kernel library (libdrk.so).
+ *
+ * One call = one segment-local operation enqueued on a CUDA stream of one device.
+ * Everything is enqueue-only and asynchronous; the caller (the Python runtime, or any
+ * other host through ctypes / cffi) owns all memory, streams and synchronisation.
+ * Pointers are raw device addresses; `stream` is a cudaStream_t passed as void*.
+ * Every entry returns 0 on success, otherwise a cudaError_t value or one of the DRK_E_*
+ * codes below; drk_last_error() then describes the failure (thread-local string).
+ * Arguments are validated before anything is enqueued ("error before any write",
+ * reference runtime.py:324-330, algorithms.py:186-187,476-477).
+ *
+ * The reference (segrange, pure Python + numpy) has no FFI; each entry point below names
+ * the per-segment numpy call site it replaces, so a maintainer can bind it there (see
+ * INTEGRATION.md for the ctypes stub a segrange task would call).
+ */
+#ifndef DRK_H
+#define DRK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* element types (numpy dtypes float32, float64, int32, int64) */
+enum { DRK_F32 = 0, DRK_F64 = 1, DRK_I32 = 2, DRK_I64 = 3 };
+/* binary operators (reference algorithms.py:47-50: add, multiply, minimum, maximum) */
+enum { DRK_ADD = 0, DRK_MUL = 1, DRK_MIN = 2, DRK_MAX = 3 };
+/* generator kinds for drk_generate (reference repro.py:21-40) */
+enum { DRK_GEN_UNIFORM = 0, DRK_GEN_MOD = 1 };
+/* library error codes (disjoint from cudaError_t values, which stay below 1000) */
+enum { DRK_E_ARG = 1001, DRK_E_DTYPE = 1002, DRK_E_SCRATCH = 1003, DRK_E_JIT = 1004 };
+
+int drk_version(void);
+const char* drk_last_error(void);
+/* number of CUDA devices visible to this process (0 on a host without a GPU) */
+int drk_device_count(int* count);
+
+/* ---- stream plumbing (runtime.py:191-280 allocate/copy/wait_all become stream ops) ---- */
+/* cudaMemcpyAsync with cudaMemcpyDefault (host<->device, device<->device, peer over NVLink) */
+int drk_memcpy_async(void* dst, const void* src, size_t bytes, int device, void* stream);
+int drk_memset_async(void* dst, int value, size_t bytes, int device, void* stream);
+/* the wait_all barrier for one locale stream (runtime.py:229-245) */
+int drk_stream_synchronize(int device, void* stream);
+/* let kernels on `device` load/store memory of `peer` (NVLink P2P through NVSwitch) */
+int drk_enable_peer_access(int device, int peer);
+
+/* ---- elementwise (map) kernels -------------------------------------------------------
+ * Replace `VectorSegment.store_array(values)` of a materialised view
+ * (containers.py:65-67 fed by views.py:164-181 `_apply_elementwise`) and the vectorised
+ * `for_each` task (algorithms.py:101-111).  One read of each input, one write. */
+
+/* out[i] = in[i]                      — algorithms.copy aligned path, algorithms.py:493-503 */
+int drk_copy(int dtype, void* out, const void* in, int64_t n, int device, void* stream);
+/* out[i] = *value                     — DistributedVector(init=v), containers.py:110-113 */
+int drk_fill(int dtype, void* out, int64_t n, const void* value, int device, void* stream);
+/* out[i] = start + i                  — iota / views.enumerate leaf (no reference analogue) */
+int drk_iota(int dtype, void* out, int64_t n, int64_t start, int device, void* stream);
+/* out[i] = alpha * in[i]              — STREAM scale */
+int drk_scale(int dtype, void* out, const void* in, int64_t n, const void* alpha, int device,
+              void* stream);
+/* out[i] = a[i] + b[i]                — STREAM add, test_algorithms.py:25-31 */
+int drk_add(int dtype, void* out, const void* a, const void* b, int64_t n, int device,
+            void* stream);
+/* out[i] = b[i] + alpha * c[i]        — bench.stream_triad, bench.py:93-99 (two roundings) */
+int drk_triad(int dtype, void* out, const void* b, const void* c, int64_t n, const void* alpha,
+              int device, void* stream);
+/* out[i] = European call price         — bench.black_scholes_call/prices, bench.py:106-126 */
+int drk_black_scholes(int dtype, void* out, const void* spot, const void* strike,
+                      const void* rate, const void* volatility, const void* expiry, int64_t n,
+                      int device, void* stream);
+/* Device twin of repro.py:21-40 (splitmix64 window [start, start+n) of `seed`):
+ *   DRK_GEN_UNIFORM: out[i] = dtype(a + (b - a) * unit_double)   (a=0,b=1: unit_doubles)
+ *   DRK_GEN_MOD:     out[i] = dtype(int64(bits % (uint64)a) + (int64)b)
+ * bit-identical to the numpy generator followed by astype(dtype). */
+int drk_generate(int dtype, void* out, int64_t n, uint64_t seed, uint64_t start, int kind,
+                 double a, double b, int device, void* stream);
+
+/* ---- reductions ------------------------------------------------------------------------
+ * Replace `_reduce_task` (algorithms.py:153-162): `op.ufunc.reduce(eval_array())`.
+ * The result is written to `result_dev` in the accumulator type drk_acc_dtype(dtype, op)
+ * (float32 add/mul -> float64, int32 add/mul -> int64, otherwise dtype).  `scratch` must
+ * hold drk_reduce_scratch_bytes() bytes, zero-filled once at allocation; it is left
+ * zero-filled again after each call, so one scratch serves every call on one stream.
+ * n must be >= 1 (the reference drops empty segments, algorithms.py:61-71). */
+size_t drk_reduce_scratch_bytes(void);
+int drk_acc_dtype(int dtype, int op);
+int drk_reduce(int dtype, int op, const void* x, int64_t n, void* result_dev, void* scratch,
+               int device, void* stream);
+/* fused zip|transform(t[0]*t[1])|reduce(add) — bench.dot_product, bench.py:87-90 */
+int drk_dot(int dtype, const void* x, const void* y, int64_t n, void* result_dev,
+            void* scratch, int device, void* stream);
+
+/* ---- scans -----------------------------------------------------------------------------
+ * Replace `_local_scan_task` + `_offset_task` / `_seed_task` (algorithms.py:277-308) with a
+ * single-pass decoupled look-back scan; the cross-segment carry is an input instead of a
+ * second read-modify-write pass.  Values in the accumulator type A = drk_acc_dtype():
+ *   init_host     exclusive scans: host pointer to init (A), required; else NULL
+ *   carry_host    host pointer to a carry value (A), or NULL
+ *   carry_dev     device pointer to a carry value (A) written by an earlier call on the
+ *                 same stream (segment chaining), or NULL; at most one carry may be given
+ *   seg_total_dev out: this segment's total, without carry (A), or NULL
+ *   carry_out_dev out: carry ⊕ segment total (A), or NULL
+ * inclusive: out[j] = carry ⊕ in[0..j];  exclusive: out[0] = init ⊕ carry,
+ * out[j] = init ⊕ carry ⊕ in[0..j-1].  in == out (in place) is allowed.  n >= 1.
+ * `scratch` must hold drk_scan_scratch_bytes(dtype, op, n) bytes (no initialisation). */
+size_t drk_scan_scratch_bytes(int dtype, int op, int64_t n);
+int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_t n,
+             const void* init_host, const void* carry_host, const void* carry_dev,
+             void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
+             int device, void* stream);
+
+/* ---- tuning / introspection ------------------------------------------------------------ */
+/* set a launch parameter by name ("map_waves", "reduce_waves"); returns the old value */
+int drk_tune(const char* name, int value);
+/* number of kernels this library has launched in this process */
+int64_t drk_launch_count(void);
+
+/* ---- run-time compiled kernels (NVRTC) for traced view expressions ----------------------
+ * drk_jit_compile compiles CUDA C++ `source` (which may #include "drk_device.cuh" from
+ * `include_dir`) for sm_100a and loads it; `*handle` identifies the module.  drk_jit_launch
+ * launches `kernel` from that module on (device, stream) with a packed argument block
+ * (`params`, `params_bytes`, passed by value as the kernel's single argument). */
+int drk_jit_compile(const char* source, const char* name, const char* include_dir,
+                    void** handle, char* log, size_t log_bytes);
+int drk_jit_cubin(const char* source, const char* name, const char* include_dir,
+                  void* cubin_out, size_t* cubin_bytes, char* log, size_t log_bytes);
+int drk_jit_load(const void* cubin, void** handle);
+int drk_jit_launch(void* handle, const char* kernel, unsigned grid, unsigned block,
+                   unsigned smem, const void* params, size_t params_bytes, int device,
+                   void* stream);
+int drk_jit_occupancy(void* handle, const char* kernel, unsigned block, unsigned smem,
+                      int device, int* blocks_per_sm, int* sm_count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DRK_H */

@@ -1,0 +1,477 @@
+"""Segment-parallel algorithms on the device runtime.
+
+Same collective driver-side calls as the reference
+(/root/reference/pkg/src/segrange/algorithms.py): for_each (:86-128), reduce (:135-162),
+inclusive/exclusive_scan (:169-308, incl. the white-box ``_scan_aligned``), copy
+(:468-503), plus ``fill`` and ``transform`` from the north star.  The driver decomposes
+the input into segments, lowers each to a fused device expression (views.lower), and
+enqueues one kernel per segment on the segment's GPU stream; the combine steps that the
+reference runs on the driver (ascending fold of partials, scan of segment totals) stay
+on the host over P scalars, with identical numpy scalar semantics.
+
+Element functions are traced once on symbols (expr.py) instead of being executed per
+element; functions that cannot be traced raise TypeError rather than running on the
+host.
+"""
+
+from __future__ import annotations
+
+import operator
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, expr, kernels
+from . import views as _views
+from .containers import DistributedVector
+from .core import has_segments, is_aligned, runtime_of, segments_of
+from .kernels import OPCODES, Launch, run_map, run_reduce, run_scan, stage_leaves
+from .runtime import AggregateTaskError
+from .views import ReadOnly, Target, ZipView, lower
+
+
+@dataclass(frozen=True)
+class BinaryOp:
+    """A binary operator with optional identity and numpy ufunc (algorithms.py:34-44)."""
+
+    fn: callable
+    identity: object = None
+    ufunc: object = None
+    name: str = ""
+
+    def __call__(self, a, b):
+        return self.fn(a, b)
+
+
+add = BinaryOp(operator.add, 0, np.add, "add")
+multiply = BinaryOp(operator.mul, 1, np.multiply, "multiply")
+minimum = BinaryOp(min, None, np.minimum, "minimum")
+maximum = BinaryOp(max, None, np.maximum, "maximum")
+
+
+def as_binary_op(op) -> BinaryOp:
+    if isinstance(op, BinaryOp):
+        return op
+    if callable(op):
+        return BinaryOp(op)
+    raise TypeError(f"expected a BinaryOp or callable, got {type(op).__name__}")
+
+
+def _opcode(op: BinaryOp):
+    if op.ufunc is None:
+        return None
+    return OPCODES.get(getattr(op.ufunc, "__name__", ""))
+
+
+def _pieces(r) -> list:
+    """Non-empty segment pieces of r (algorithms.py:61-71)."""
+    if has_segments(r) or isinstance(r, ZipView):
+        segs = r.segments() if isinstance(r, ZipView) else segments_of(r)
+    else:
+        segs = [_views._as_piece(r, len(r))]
+    return [s for s in segs if len(s)]
+
+
+def _require_runtime(rt, what):
+    if rt is None:
+        raise TypeError(f"{what}: input has no device runtime (plain host data); build a DistributedVector")
+    rt._check_compute()
+    return rt
+
+
+def _launch_for(rt, rank):
+    return Launch(rt.state_of(rank if rank is not None else 0))
+
+
+def _promote_python(value):
+    """Element-wise (non-vectorised) functions see Python scalars in the reference
+    (`seg.get(i)` -> .item()): float32 -> float, int32 -> int."""
+    if value is None:
+        return None
+    if isinstance(value, tuple):
+        return tuple(_promote_python(v) for v in value)
+    dt = value.dtype
+    if dt.kind == "f" and dt != np.float64:
+        return expr.cast(value, np.float64)
+    if dt.kind in "iu" and dt != np.int64:
+        return expr.cast(value, np.int64)
+    return value
+
+
+# ----------------------------------------------------------------------------------------
+# for_each
+
+
+def for_each(r, fn, vectorized: bool = False) -> None:
+    """Apply fn to every element; its non-None result replaces the element (a tuple for
+    zips, None components skipped).  Effects are visible on return (algorithms.py:86-98)."""
+    pieces = _pieces(r)
+    if not pieces:
+        return
+    rt = _require_runtime(runtime_of(r), "for_each")
+    cache = {}
+    launches = []
+    for piece in pieces:
+        lw = lower(piece)
+        value = lw.value if vectorized else _promote_python(lw.value)
+        key = _views._value_key(value)
+        if key not in cache:
+            cache[key] = expr.trace(fn, value)
+        result = cache[key]
+        if result is None:
+            raise TypeError(
+                "for_each function returned None for every element: it only has side effects, which "
+                "cannot run inside a device kernel"
+            )
+        writes = []
+        _collect_writes(result, lw.target, writes)
+        if not writes:
+            continue
+        launch = _launch_for(rt, writes[0][0].handle.locale)
+        run_map(writes, lw.leaves, lw.length, launch)
+        launches.append(launch)
+    _finish(rt, launches)
+
+
+def _collect_writes(result, target, writes):
+    if result is None:
+        return
+    if isinstance(target, ReadOnly):
+        raise TypeError(f"cannot write through read-only {target.what}")
+    if isinstance(target, tuple):
+        if not isinstance(result, tuple) or len(result) != len(target):
+            n = len(target)
+            raise ValueError(f"expected a {n}-tuple, got {len(result) if isinstance(result, tuple) else 1} values")
+        for r, t in zip(result, target):
+            _collect_writes(r, t, writes)
+        return
+    if isinstance(result, tuple):
+        raise TypeError("element function returned a tuple for a non-zip range")
+    writes.append((target, result))
+
+
+def _finish(rt, launches):
+    devs = {id(l.state): l.state for l in launches}
+    for st in devs.values():
+        st.synchronize()
+
+
+# ----------------------------------------------------------------------------------------
+# reduce
+
+
+def _partial_dtype(op: BinaryOp, dtype):
+    """numpy's reduce result dtype (int32 add/mul -> int64, float32 stays float32)."""
+    if op.ufunc is not None:
+        return op.ufunc.reduce(np.zeros(1, dtype=dtype)).dtype
+    return np.dtype(dtype)
+
+
+def reduce(r, init=0, op=add):
+    """Fold all elements onto init: per-segment device partials, then an ascending fold on
+    the driver (algorithms.py:135-150), so exact types give identical results for every
+    segment count."""
+    op = as_binary_op(op)
+    pieces = _pieces(r)
+    if not pieces:
+        return init.item() if isinstance(init, np.generic) else init
+    rt = _require_runtime(runtime_of(r), "reduce")
+    partials = _segment_partials(rt, pieces, op)
+    acc = init
+    for p in partials:
+        acc = op.fn(acc, p)
+    return acc.item() if isinstance(acc, np.generic) else acc
+
+
+def _segment_partials(rt, pieces, op):
+    opcode = _opcode(op)
+    lowered = []
+    for piece in pieces:
+        lw = lower(piece)
+        if isinstance(lw.value, tuple):
+            raise TypeError("reduce needs scalar elements; apply a transform to the zip first")
+        lowered.append(lw)
+    combiner = None
+    if opcode is None:
+        combiner = op  # traced by codegen per value dtype
+    need = {}
+    for lw in lowered:
+        st = rt.state_of(lw.rank if lw.rank is not None else 0)
+        need[id(st)] = (st, need.get(id(st), (st, 0))[1] + 1)
+    for st, k in need.values():
+        st.ensure_results(k)  # before any launch: growing the slot buffer reallocates it
+    slots = {}
+    order = []
+    launches = {}
+    for lw in lowered:
+        st = rt.state_of(lw.rank if lw.rank is not None else 0)
+        launch = launches.setdefault(id(st), Launch(st))
+        slot = slots.get(id(st), 0)
+        slots[id(st)] = slot + 1
+        node = lw.value if opcode is not None else _promote_python(lw.value)
+        run_reduce(node, lw.leaves, lw.length, opcode, combiner, launch, slot)
+        order.append((st, slot, node.dtype))
+    raw = {id(l.state): l.state.fetch_results(slots[id(l.state)]) for l in launches.values()}
+    out = []
+    for st, slot, vdt in order:
+        if opcode is not None:
+            A = _lib.acc_dtype(vdt, opcode)
+            a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + A.itemsize].tobytes(), dtype=A)[0]
+            out.append(a.astype(_partial_dtype(op, vdt)))
+        else:
+            a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + vdt.itemsize].tobytes(), dtype=vdt)[0]
+            out.append(a.item())
+    return out
+
+
+# ----------------------------------------------------------------------------------------
+# scans
+
+
+def inclusive_scan(r, out, op=add) -> None:
+    """out[i] = fold of r[0..i] (algorithms.py:169-177)."""
+    _scan_entry(r, out, as_binary_op(op), exclusive=False, init=None)
+
+
+def exclusive_scan(r, out, init, op=add) -> None:
+    """out[0] = init, out[i] = init ⊕ fold of r[0..i) (algorithms.py:180-182)."""
+    _scan_entry(r, out, as_binary_op(op), exclusive=True, init=init)
+
+
+def _scan_entry(r, out, op, exclusive, init):
+    if len(r) != len(out):
+        raise ValueError(f"scan length mismatch: input {len(r)}, output {len(out)}")
+    r_seg, o_seg = has_segments(r), has_segments(out)
+    if not o_seg:
+        raise TypeError("scan output must be a segmented device range")
+    if r is out or (r_seg and is_aligned(r, out)):
+        _scan_aligned(r, out, op, exclusive, init)
+        return
+    if not isinstance(out, DistributedVector):
+        raise TypeError("non-aligned scan needs a DistributedVector output")
+    temp = DistributedVector.like_distribution(out.runtime, out.distribution, out.dtype)
+    copy(r, temp)
+    _scan_aligned(temp, out, op, exclusive, init)
+
+
+def _scan_aligned(r, out, op, exclusive, init) -> list:
+    """Aligned scan; returns the per-segment input totals (None for empty segments), the
+    white-box intermediate of the reference (algorithms.py:234-274)."""
+    return _scan_impl(r, out, op, exclusive, init)
+
+
+def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
+    """Aligned scan with an optional incoming carry (the fold of everything before r,
+    in the accumulator type; used when r is one rank's block of a larger vector)."""
+    op = as_binary_op(op)
+    in_segs = segments_of(r)
+    out_segs = segments_of(out)
+    live = [k for k, s in enumerate(in_segs) if len(s)]
+    partials = [None] * len(in_segs)
+    if not live:
+        return partials
+    rt = _require_runtime(runtime_of(out, r), "scan")
+    opcode = _opcode(op)
+    if opcode is None:
+        from . import codegen
+
+        return codegen.custom_scan(rt, in_segs, out_segs, live, op, exclusive, init, carry)
+
+    # 1. bring every live input segment into its output segment's dtype/buffer if it is a
+    #    view (materialise into `out`, then scan in place); plain vectors scan in -> out.
+    work = []
+    launches = {}
+    for k in live:
+        lw = lower(in_segs[k])
+        tgt = lower(out_segs[k]).target
+        if not isinstance(tgt, Target):
+            raise TypeError("scan output segments must be writable vector storage")
+        st = rt.state_of(out_segs[k].rank)
+        launch = launches.setdefault(id(st), Launch(st))
+        node = lw.value
+        if isinstance(node, tuple):
+            raise TypeError("scan needs scalar elements; apply a transform to the zip first")
+        plain = node.op == "leaf" and lw.leaves[node.value].kind == "array" and node.dtype == tgt.dtype
+        if plain and lw.leaves[node.value].device == st.index:
+            in_ptr = lw.leaves[node.value].ptr()
+        else:
+            run_map([(tgt, node)], lw.leaves, lw.length, launch)
+            in_ptr = tgt.ptr()
+        work.append((k, st, launch, in_ptr, tgt))
+
+    T = np.dtype(out.dtype if hasattr(out, "dtype") else work[0][4].dtype)
+    A = _lib.acc_dtype(T, opcode)
+    L = _partial_dtype(op, T)
+    devices = {id(w[1]) for w in work}
+    init_a = None
+    if exclusive:
+        init_a = _to_acc(init, A)
+
+    if len(devices) == 1:
+        # single device: chain the carry on the device, one pass per segment
+        st = work[0][1]
+        st.ensure_results(2 * len(work) + 2)
+        prev_carry = None
+        for j, (k, _, launch, in_ptr, tgt) in enumerate(work):
+            first_carry = _to_acc(carry, A) if (j == 0 and carry is not None) else None
+            run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a,
+                     carry_value=first_carry,
+                     carry_dev=st.result_dev_ptr(prev_carry) if prev_carry is not None else None,
+                     seg_total_slot=2 * j, carry_out_slot=2 * j + 1)
+            prev_carry = 2 * j + 1
+        raw = st.fetch_results(2 * len(work))
+        for j, (k, *_rest) in enumerate(work):
+            total = np.frombuffer(raw[16 * j : 16 * j + A.itemsize].tobytes(), dtype=A)[0]
+            partials[k] = total.astype(L).item()
+        _check_carry_range(op, partials, live, exclusive, init, T, carry)
+        return partials
+
+    # several devices: totals first (all GPUs in parallel), carries on the host exactly as
+    # the reference's driver loop, then one carried scan per segment.
+    per_dev_slot = {}
+    for k, st, launch, in_ptr, tgt in work:
+        per_dev_slot[id(st)] = per_dev_slot.get(id(st), 0) + 1
+    for k, st, *_ in work:
+        st.ensure_results(per_dev_slot[id(st)])
+    per_dev_slot = {}
+    for k, st, launch, in_ptr, tgt in work:
+        slot = per_dev_slot.get(id(st), 0)
+        per_dev_slot[id(st)] = slot + 1
+        kernels.launch_kernel("drk_reduce", launch, tgt.length, _lib.dtype_code(T), opcode, in_ptr, tgt.length,
+                       st.result_dev_ptr(slot), st.reduce_scratch.data_ptr())
+    fetched = {id(w[1]): w[1].fetch_results(per_dev_slot[id(w[1])]) for w in work}
+    counter = {}
+    for k, st, *_ in work:
+        slot = counter.get(id(st), 0)
+        counter[id(st)] = slot + 1
+        total = np.frombuffer(fetched[id(st)][8 * slot : 8 * slot + A.itemsize].tobytes(), dtype=A)[0]
+        partials[k] = total.astype(L).item()
+    offsets = _offsets(op, partials, carry)
+    _check_carry_range(op, partials, live, exclusive, init, T, carry)
+    for k, st, launch, in_ptr, tgt in work:
+        off = offsets[k]
+        run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a,
+                 carry_value=_to_acc(off, A) if off is not None else None)
+    for l in launches.values():
+        l.state.synchronize()
+    return partials
+
+
+def _to_acc(v, A):
+    return np.asarray(v).astype(A).item() if np.asarray(v).dtype != A else np.asarray(v).item()
+
+
+def _offsets(op, partials, carry=None):
+    offsets, prefix = [], carry
+    for p in partials:
+        offsets.append(prefix)
+        if p is not None:
+            prefix = p if prefix is None else op.fn(prefix, p)
+    return offsets
+
+
+def _check_carry_range(op, partials, live, exclusive, init, T, carry=None):
+    """The reference adds the (Python int) carry to an int32 segment with np.add, which
+    raises OverflowError once the carry leaves the int32 range (algorithms.py:292-308)."""
+    if T.kind not in "iu" or T.itemsize >= 8:
+        return
+    info = np.iinfo(T)
+    offsets = _offsets(op, partials, carry)
+    failures = []
+    for j, k in enumerate(live):
+        off = offsets[k]
+        seed = off
+        if exclusive:
+            seed = init if off is None else op.fn(init, off)
+        if seed is None:
+            continue
+        if not info.min <= int(seed) <= info.max:
+            failures.append((j, OverflowError(f"Python integer {int(seed)} out of bounds for {T}")))
+    if failures:
+        raise AggregateTaskError(failures)
+
+
+# ----------------------------------------------------------------------------------------
+# copy / fill / transform
+
+
+def copy(src, dst) -> None:
+    """Element copy between equal-length ranges: aligned pairs segment by segment, else
+    chunks at the union of both sides' boundaries (algorithms.py:468-503).  Sources may
+    be lazy views (fused into the copy kernel); host arrays on either side are
+    transferred over PCIe."""
+    if len(src) != len(dst):
+        raise ValueError(f"copy length mismatch: source {len(src)}, destination {len(dst)}")
+    if len(src) == 0:
+        return
+    rt = runtime_of(dst, src)
+    s_seg, d_seg = has_segments(src), has_segments(dst)
+    if s_seg and d_seg and is_aligned(src, dst):
+        pairs = [(s, d) for s, d in zip(segments_of(src), segments_of(dst)) if len(s)]
+    else:
+        src_list = segments_of(src) if s_seg else [_views._as_piece(src, len(src))]
+        dst_list = segments_of(dst) if d_seg else [_views._as_piece(dst, len(dst))]
+        pairs = [tuple(ch.components) for ch in _views.realign_segments([src_list, dst_list])]
+    rt = _require_runtime(rt, "copy")
+    launches = []
+    for s, d in pairs:
+        ls = lower(s)
+        if isinstance(ls.value, tuple):
+            raise TypeError("copy source elements must be scalars")
+        if isinstance(d, _views.LocalPiece):
+            _copy_to_host(rt, ls, d, launches)
+            continue
+        tgt = lower(d).target
+        if isinstance(tgt, ReadOnly):
+            raise TypeError(f"cannot write through read-only {tgt.what}")
+        launch = Launch(rt.state_of(d.rank))
+        run_map([(tgt, ls.value)], ls.leaves, ls.length, launch)
+        launches.append(launch)
+    _finish(rt, launches)
+
+
+def _copy_to_host(rt, ls, piece, launches):
+    if not piece.writable:
+        raise TypeError("cannot write through a sequence converted to a local piece")
+    node = ls.value
+    rank = ls.rank if ls.rank is not None else 0
+    st = rt.state_of(rank)
+    launch = Launch(st)
+    host = piece.array
+    if node.op == "leaf" and ls.leaves[node.value].kind == "array" and node.dtype == host.dtype \
+            and host.flags.c_contiguous:
+        _lib.call("drk_memcpy_async", host.ctypes.data, ls.leaves[node.value].ptr(), host.nbytes, st.index,
+                  st.handle)
+        st.synchronize()
+        return
+    from .runtime import torch, torch_dtype
+
+    t = torch()
+    with t.cuda.stream(st.stream):
+        tmp = t.empty(ls.length, dtype=torch_dtype(host.dtype), device=st.device)
+    h = _views.Target.__new__(_views.Target)
+    h.handle, h.start, h.length, h.dtype = _TmpHandle(tmp, st.index), 0, ls.length, np.dtype(host.dtype)
+    run_map([(h, node)], ls.leaves, ls.length, launch)
+    st.synchronize()
+    host[...] = tmp.cpu().numpy()
+
+
+class _TmpHandle:
+    def __init__(self, tensor, device):
+        self._t = tensor
+        self.device_index = device
+        self.locale = None
+
+    def data_ptr(self):
+        return self._t.data_ptr()
+
+
+def fill(r, value) -> None:
+    """Set every element of a writable range to value."""
+    for_each(r, lambda _x: value, vectorized=True)
+
+
+def transform(src, dst, fn) -> None:
+    """dst[i] = fn(src[i]) — the reference spells this copy(views.transform(src, fn), dst)
+    (algorithms.py:468-503, tests/test_algorithms.py:376-381)."""
+    copy(_views.transform(src, fn), dst)

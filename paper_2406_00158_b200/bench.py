@@ -1,0 +1,297 @@
+"""Benchmark kernels of the distributed-ranges paper on the device runtime.
+
+Same kernels and harness as the reference's bench module
+(/root/reference/pkg/src/segrange/bench.py): dot_product = zip|transform|reduce
+(:87-90), stream_triad (:93-99), Black-Scholes (:102-126), BenchSpec / run_spec / CSV
+(:50-80, 348-386); plus the other STREAM kernels (copy, scale, add) named by the north
+star.  Each kernel here is the *same view pipeline* as the reference, lowered to one
+fused sm_100a kernel per segment.  GEMM and sort are outside this runtime's scope.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib, algorithms, expr, repro, views
+from .algorithms import add
+from .containers import DistributedVector
+from .runtime import Runtime
+from .views import get_zip_mode, set_zip_mode
+
+BENCH_NAMES = ("dot", "reduce", "inclusive_scan", "black_scholes", "stream")
+DEFAULT_SIZES = {name: 10**7 for name in BENCH_NAMES}
+REL_TOL = 1e-12
+STREAM_ALPHA = 3.0
+
+# Strike below spot keeps prices O(10), so relative tolerances are meaningful (bench.py:39-47).
+BS_RANGES = {
+    "spot": (90.0, 110.0),
+    "strike": (70.0, 90.0),
+    "rate": (0.0, 0.05),
+    "volatility": (0.1, 0.4),
+    "expiry": (0.25, 2.0),
+}
+
+
+@dataclass(frozen=True)
+class BenchSpec:
+    name: str
+    size: int
+    locales: int
+    reps: int = 3
+    seed: int = 1
+    check: bool = False
+    mode: str = "relaxed"
+    dtype: str = "float64"
+
+    def __post_init__(self):
+        if self.name not in BENCH_NAMES:
+            raise ValueError(f"unknown bench {self.name!r}; one of {BENCH_NAMES}")
+        if self.reps < 1:
+            raise ValueError("reps must be at least 1")
+        if self.size < 0:
+            raise ValueError("size must be non-negative")
+
+
+@dataclass
+class BenchResult:
+    spec: BenchSpec
+    seconds: list = field(default_factory=list)
+    checksum: str = ""
+    verified: bool | None = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def median_seconds(self) -> float:
+        s = sorted(self.seconds)
+        return s[len(s) // 2] if s else float("nan")
+
+
+# ----------------------------------------------------------------------------------------
+# kernels (the same view pipelines as the reference)
+
+
+def dot_product(x, y):
+    """zip | transform(t[0]*t[1]) | reduce(add) — one fused kernel per segment."""
+    z = views.transform(views.zip(x, y), lambda t: t[0] * t[1])
+    return algorithms.reduce(z, 0.0, add)
+
+
+def stream_triad(a, b, c, alpha=STREAM_ALPHA):
+    """a[i] = b[i] + alpha * c[i]."""
+    algorithms.for_each(views.zip(a, b, c), lambda t: (t[1] + alpha * t[2], None, None), vectorized=True)
+
+
+def stream_copy(c, a):
+    """c[i] = a[i]."""
+    algorithms.copy(a, c)
+
+
+def stream_scale(b, c, alpha=STREAM_ALPHA):
+    """b[i] = alpha * c[i]."""
+    algorithms.for_each(views.zip(b, c), lambda t: (alpha * t[1], None), vectorized=True)
+
+
+def stream_add(c, a, b):
+    """c[i] = a[i] + b[i]."""
+    algorithms.for_each(views.zip(c, a, b), lambda t: (t[1] + t[2], None, None), vectorized=True)
+
+
+def _bs_result_dtype(dts):
+    return np.float32 if all(np.dtype(d) == np.float32 for d in dts) else np.float64
+
+
+def _bs_host(spot, strike, rate, volatility, expiry):
+    """black_scholes_call on plain scalars/arrays: evaluated by the device kernel."""
+    from .runtime import torch
+
+    args = [np.atleast_1d(np.asarray(a, dtype=np.float64)) for a in (spot, strike, rate, volatility, expiry)]
+    shape = np.broadcast_shapes(*[a.shape for a in args])
+    args = [np.ascontiguousarray(np.broadcast_to(a, shape)).ravel() for a in args]
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("black_scholes_call needs a CUDA device (no CPU fallback)")
+    dev = t.device("cuda", t.cuda.current_device())
+    d_in = [t.from_numpy(a).to(dev) for a in args]
+    d_out = t.empty(args[0].size, dtype=t.float64, device=dev)
+    stream = t.cuda.current_stream(dev)
+    _lib.call("drk_black_scholes", _lib.F64, d_out.data_ptr(), *[x.data_ptr() for x in d_in], args[0].size,
+              dev.index, stream.cuda_stream)
+    stream.synchronize()
+    out = d_out.cpu().numpy().reshape(shape)
+    return out if np.ndim(spot) else out.reshape(np.shape(spot) if np.ndim(spot) else ())
+
+
+black_scholes_call = expr.DeviceFunction("black_scholes", 5, _bs_result_dtype, _bs_host)
+black_scholes_call.__doc__ = """European call price C = S*Phi(d1) - K*exp(-rT)*Phi(d2); vol = sigma*sqrt(T) <= 0
+gives the discounted intrinsic value (reference bench.py:106-116).  Inside a traced
+element function it becomes the fused drk_black_scholes kernel."""
+
+
+def norm_cdf(x):
+    from scipy.special import erf
+
+    return 0.5 * (1.0 + erf(x / np.sqrt(2.0)))
+
+
+def black_scholes_prices(out, spot, strike, rate, volatility, expiry):
+    """out[i] = call price of option i, element-wise over the zipped inputs."""
+    algorithms.for_each(
+        views.zip(out, spot, strike, rate, volatility, expiry),
+        lambda t: (black_scholes_call(t[1], t[2], t[3], t[4], t[5]), None, None, None, None, None),
+        vectorized=True,
+    )
+
+
+# ----------------------------------------------------------------------------------------
+# sequential oracles for --check (plain loops on host copies; verification only)
+
+
+def _oracle_dot(xs, ys) -> float:
+    total = 0.0
+    for a, b in zip(xs.tolist(), ys.tolist()):
+        total += a * b
+    return total
+
+
+def _oracle_bs(S, K, r, v, T) -> float:
+    vol = v * math.sqrt(T)
+    disc = math.exp(-r * T)
+    if vol <= 0.0:
+        return max(S - K * disc, 0.0)
+    d1 = (math.log(S / K) + (r + 0.5 * v * v) * T) / vol
+    d2 = d1 - vol
+    phi = lambda x: 0.5 * (1.0 + math.erf(x / math.sqrt(2.0)))
+    return S * phi(d1) - K * disc * phi(d2)
+
+
+def rel_close(actual, expected, tol) -> bool:
+    return bool(np.isclose(np.asarray(actual), np.asarray(expected), rtol=tol, atol=0.0).all())
+
+
+def _timed(reps, kernel):
+    seconds, result = [], None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        result = kernel()
+        seconds.append(time.perf_counter() - t0)
+    return seconds, result
+
+
+def _dt(spec):
+    return np.dtype(spec.dtype)
+
+
+def bench_dot(spec: BenchSpec, rt: Runtime) -> BenchResult:
+    n, dt = spec.size, _dt(spec)
+    xs = repro.unit_doubles(spec.seed, 0, n).astype(dt)
+    ys = repro.unit_doubles(spec.seed, n, n).astype(dt)
+    x = DistributedVector.from_numpy(rt, xs)
+    y = DistributedVector.from_numpy(rt, ys)
+    seconds, value = _timed(spec.reps, lambda: dot_product(x, y))
+    res = BenchResult(spec, seconds, repro.checksum(np.float64(value)))
+    if spec.check:
+        tol = REL_TOL if dt == np.float64 else 1e-5
+        res.verified = rel_close(value, _oracle_dot(xs, ys), tol) if n else value == 0.0
+    return res
+
+
+def bench_reduce(spec: BenchSpec, rt: Runtime) -> BenchResult:
+    n = spec.size
+    v = DistributedVector(rt, n, dtype=np.int64)
+    if n:
+        algorithms.copy(views.iota(n), v)
+    seconds, value = _timed(spec.reps, lambda: algorithms.reduce(v, 0, add))
+    res = BenchResult(spec, seconds, repro.checksum(np.int64(value)))
+    if spec.check:
+        res.verified = value == n * (n - 1) // 2
+    return res
+
+
+def bench_inclusive_scan(spec: BenchSpec, rt: Runtime) -> BenchResult:
+    n = spec.size
+    v = DistributedVector(rt, n, dtype=np.int64)
+    if n:
+        algorithms.copy(views.iota(n), v)
+    out = DistributedVector(rt, n, init=0, dtype=np.int64)
+    seconds, _ = _timed(spec.reps, lambda: algorithms.inclusive_scan(v, out, add))
+    data = out.to_numpy()
+    res = BenchResult(spec, seconds, repro.checksum(data))
+    if spec.check:
+        i = np.arange(n, dtype=np.int64)
+        res.verified = bool(np.array_equal(data, i * (i + 1) // 2))
+    return res
+
+
+def bench_black_scholes(spec: BenchSpec, rt: Runtime) -> BenchResult:
+    n, dt = spec.size, _dt(spec)
+    cols = {name: repro.uniform_doubles(spec.seed, k * n, n, lo, hi).astype(dt)
+            for k, (name, (lo, hi)) in enumerate(BS_RANGES.items())}
+    vecs = {k: DistributedVector.from_numpy(rt, v) for k, v in cols.items()}
+    out = DistributedVector(rt, n, dtype=dt)
+    seconds, _ = _timed(spec.reps, lambda: black_scholes_prices(
+        out, vecs["spot"], vecs["strike"], vecs["rate"], vecs["volatility"], vecs["expiry"]))
+    data = out.to_numpy()
+    res = BenchResult(spec, seconds, repro.checksum(data))
+    if spec.check:
+        exp = np.array([_oracle_bs(*(float(cols[k][i]) for k in BS_RANGES)) for i in range(n)])
+        res.verified = rel_close(data, exp, REL_TOL if dt == np.float64 else 1e-5)
+    return res
+
+
+def bench_stream(spec: BenchSpec, rt: Runtime) -> BenchResult:
+    n, dt = spec.size, _dt(spec)
+    bs = repro.unit_doubles(spec.seed, 0, n).astype(dt)
+    cs = repro.unit_doubles(spec.seed, n, n).astype(dt)
+    a = DistributedVector(rt, n, dtype=dt)
+    b = DistributedVector.from_numpy(rt, bs)
+    c = DistributedVector.from_numpy(rt, cs)
+    seconds, _ = _timed(spec.reps, lambda: stream_triad(a, b, c))
+    data = a.to_numpy()
+    res = BenchResult(spec, seconds, repro.checksum(data))
+    med = sorted(seconds)[len(seconds) // 2]
+    res.extra["bytes_per_second"] = 3.0 * dt.itemsize * n / med if med > 0 else float("inf")
+    if spec.check:
+        alpha = dt.type(STREAM_ALPHA)
+        res.verified = bool(np.array_equal(data, bs + alpha * cs))
+    return res
+
+
+BENCHES = {
+    "dot": bench_dot,
+    "reduce": bench_reduce,
+    "inclusive_scan": bench_inclusive_scan,
+    "black_scholes": bench_black_scholes,
+    "stream": bench_stream,
+}
+
+
+def run_spec(spec: BenchSpec) -> BenchResult:
+    previous = get_zip_mode()
+    set_zip_mode(spec.mode)
+    try:
+        with Runtime(spec.locales) as rt:
+            return BENCHES[spec.name](spec, rt)
+    finally:
+        set_zip_mode(previous)
+
+
+CSV_HEADER = "bench,size,locales,rep,seconds,checksum,verified"
+
+
+def csv_rows(results) -> list:
+    rows = [CSV_HEADER]
+    for r in results:
+        for i, sec in enumerate(r.seconds):
+            verified = "" if r.verified is None else ("true" if r.verified else "false")
+            rows.append(f"{r.spec.name},{r.spec.size},{r.spec.locales},{i},{sec:.9f},{r.checksum},{verified}")
+    return rows
+
+
+def emit_csv(results, path) -> None:
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("\n".join(csv_rows(results)) + "\n")

@@ -1,0 +1,737 @@
+// drk_kernels.cu — ahead-of-time sm_100a kernels and the C ABI declared in include/drk.h.
+//
+// Hot-path kernels of the distributed-ranges shp runtime (reference: segrange, pure
+// Python/numpy; see the per-entry citations in include/drk.h).  All kernels are
+// HBM-bandwidth bound streaming kernels; nothing here is a contraction, so there are no
+// tensor-core paths.  Template machinery lives in drk_device.cuh (shared with NVRTC).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "../../include/drk.h"
+#include "drk_device.cuh"
+
+using namespace drk;
+
+// ---------------------------------------------------------------------------------------
+// error plumbing
+
+static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+static int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+static int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return 0;
+  return set_error((int)e, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define DRK_CHECK(call)                                  \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_status(_e, #call); \
+  } while (0)
+
+extern "C" const char* drk_last_error(void) { return g_last_error.c_str(); }
+extern "C" int drk_version(void) { return 1; }
+extern "C" int64_t drk_launch_count(void) { return g_launches.load(); }
+extern "C" int64_t drk_note_launch(void) { return g_launches.fetch_add(1) + 1; }
+
+extern "C" int drk_memcpy_async(void* dst, const void* src, size_t bytes, int device, void* stream) {
+  if (bytes == 0) return 0;
+  if (!dst || !src) return set_error(DRK_E_ARG, "drk_memcpy_async: null pointer");
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) DRK_CHECK(cudaSetDevice(device));
+  DRK_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return 0;
+}
+
+extern "C" int drk_memset_async(void* dst, int value, size_t bytes, int device, void* stream) {
+  if (bytes == 0) return 0;
+  if (!dst) return set_error(DRK_E_ARG, "drk_memset_async: null pointer");
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) DRK_CHECK(cudaSetDevice(device));
+  DRK_CHECK(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream));
+  return 0;
+}
+
+extern "C" int drk_stream_synchronize(int device, void* stream) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) DRK_CHECK(cudaSetDevice(device));
+  DRK_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+extern "C" int drk_enable_peer_access(int device, int peer) {
+  int can = 0;
+  DRK_CHECK(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return set_error(DRK_E_ARG, "drk_enable_peer_access: devices cannot access each other");
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) DRK_CHECK(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return 0;
+  }
+  return cuda_status(e, "cudaDeviceEnablePeerAccess");
+}
+
+extern "C" int drk_device_count(int* count) {
+  if (!count) return set_error(DRK_E_ARG, "drk_device_count: null count");
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    *count = 0;
+    return 0;
+  }
+  return cuda_status(e, "cudaGetDeviceCount");
+}
+
+// ---------------------------------------------------------------------------------------
+// launch geometry
+
+static constexpr int BLOCK = 256;
+static constexpr int MAP_U = 4;
+static constexpr int RED_U = 4;
+static constexpr int MAX_RED_GRID = 4096;
+
+static std::mutex g_mu;
+static int g_map_waves = 0;     // 0: size grid to cover the work once (non-persistent)
+static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
+
+extern "C" int drk_tune(const char* name, int value) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!name) return -1;
+  int old = -1;
+  if (!strcmp(name, "map_waves")) {
+    old = g_map_waves;
+    g_map_waves = value;
+  } else if (!strcmp(name, "reduce_waves")) {
+    old = g_reduce_waves;
+    g_reduce_waves = value;
+  }
+  return old;
+}
+
+static int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+template <class K> static int occupancy(K kernel, int block, size_t smem) {
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = cache.find((const void*)kernel);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, smem) != cudaSuccess || n < 1)
+    n = 1;
+  cache[(const void*)kernel] = n;
+  return n;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static int prologue(int device, const char* what) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_status(e, what);
+  }
+  return 0;
+}
+
+static int epilogue(const char* what) {
+  g_launches.fetch_add(1);
+  return cuda_status(cudaGetLastError(), what);
+}
+
+// ---------------------------------------------------------------------------------------
+// map functors
+
+template <class T> struct CopyF {
+  struct Params {
+    T* out;
+    const T* in;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {
+    T a[E];
+  };
+  static __device__ __forceinline__ void load(const Params& p, i64 i, Regs& r) { ldv<T, E>(p.in + i, r.a); }
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs& r) { stv<T, E>(p.out + i, r.a); }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) { p.out[i] = p.in[i]; }
+};
+
+template <class T> struct FillF {
+  struct Params {
+    T* out;
+    T value;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {};
+  static __device__ __forceinline__ void load(const Params&, i64, Regs&) {}
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs&) {
+    T a[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[e] = p.value;
+    stv<T, E>(p.out + i, a);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) { p.out[i] = p.value; }
+};
+
+template <class T> struct IotaF {
+  struct Params {
+    T* out;
+    i64 start;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {};
+  static __device__ __forceinline__ void load(const Params&, i64, Regs&) {}
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs&) {
+    T a[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[e] = (T)(p.start + i + e);
+    stv<T, E>(p.out + i, a);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) { p.out[i] = (T)(p.start + i); }
+};
+
+template <class T> struct ScaleF {
+  struct Params {
+    T* out;
+    const T* in;
+    T alpha;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {
+    T a[E];
+  };
+  static __device__ __forceinline__ void load(const Params& p, i64 i, Regs& r) { ldv<T, E>(p.in + i, r.a); }
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs& r) {
+    T o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = Arith<T>::mul(p.alpha, r.a[e]);
+    stv<T, E>(p.out + i, o);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) {
+    p.out[i] = Arith<T>::mul(p.alpha, p.in[i]);
+  }
+};
+
+template <class T> struct AddF {
+  struct Params {
+    T* out;
+    const T* a;
+    const T* b;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {
+    T a[E], b[E];
+  };
+  static __device__ __forceinline__ void load(const Params& p, i64 i, Regs& r) {
+    ldv<T, E>(p.a + i, r.a);
+    ldv<T, E>(p.b + i, r.b);
+  }
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs& r) {
+    T o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = Arith<T>::add(r.a[e], r.b[e]);
+    stv<T, E>(p.out + i, o);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) {
+    p.out[i] = Arith<T>::add(p.a[i], p.b[i]);
+  }
+};
+
+// a = b + alpha * c with numpy's two roundings (weak-scalar alpha already in T).
+template <class T> struct TriadF {
+  struct Params {
+    T* out;
+    const T* b;
+    const T* c;
+    T alpha;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {
+    T b[E], c[E];
+  };
+  static __device__ __forceinline__ void load(const Params& p, i64 i, Regs& r) {
+    ldv<T, E>(p.b + i, r.b);
+    ldv<T, E>(p.c + i, r.c);
+  }
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs& r) {
+    T o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = Arith<T>::add(r.b[e], Arith<T>::mul(p.alpha, r.c[e]));
+    stv<T, E>(p.out + i, o);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) {
+    p.out[i] = Arith<T>::add(p.b[i], Arith<T>::mul(p.alpha, p.c[i]));
+  }
+};
+
+// Black-Scholes call (bench.py:102-116): vol = sigma*sqrt(T), disc = exp(-rT),
+// d1 = (log(S/K) + (r + sigma^2/2) T) / vol, d2 = d1 - vol,
+// price = S*Phi(d1) - K*disc*Phi(d2), Phi(x) = (1 + erf(x/sqrt 2))/2; vol <= 0 gives the
+// discounted intrinsic value max(S - K*disc, 0).  Computed in the element type.
+template <class T> struct BSMath;
+template <> struct BSMath<float> {
+  static __device__ __forceinline__ float price(float S, float K, float r, float v, float t) {
+    const float vol = v * sqrtf(t);
+    const float disc = expf(-r * t);
+    if (!(vol > 0.0f)) return fmaxf(S - K * disc, 0.0f);
+    const float d1 = (logf(S / K) + (r + 0.5f * v * v) * t) / vol;
+    const float d2 = d1 - vol;
+    const float n1 = 0.5f * (1.0f + erff(d1 * 0.70710678118654752f));
+    const float n2 = 0.5f * (1.0f + erff(d2 * 0.70710678118654752f));
+    return S * n1 - K * disc * n2;
+  }
+};
+template <> struct BSMath<double> {
+  static __device__ __forceinline__ double price(double S, double K, double r, double v, double t) {
+    const double vol = v * sqrt(t);
+    const double disc = exp(-r * t);
+    if (!(vol > 0.0)) return fmax(S - K * disc, 0.0);
+    const double d1 = (log(S / K) + (r + 0.5 * v * v) * t) / vol;
+    const double d2 = d1 - vol;
+    const double n1 = 0.5 * (1.0 + erf(d1 / 1.4142135623730951));
+    const double n2 = 0.5 * (1.0 + erf(d2 / 1.4142135623730951));
+    return S * n1 - K * disc * n2;
+  }
+};
+
+template <class T> struct BlackScholesF {
+  struct Params {
+    T* out;
+    const T *S, *K, *r, *v, *t;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {
+    T S[E], K[E], r[E], v[E], t[E];
+  };
+  static __device__ __forceinline__ void load(const Params& p, i64 i, Regs& g) {
+    ldv<T, E>(p.S + i, g.S);
+    ldv<T, E>(p.K + i, g.K);
+    ldv<T, E>(p.r + i, g.r);
+    ldv<T, E>(p.v + i, g.v);
+    ldv<T, E>(p.t + i, g.t);
+  }
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs& g) {
+    T o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = BSMath<T>::price(g.S[e], g.K[e], g.r[e], g.v[e], g.t[e]);
+    stv<T, E>(p.out + i, o);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) {
+    p.out[i] = BSMath<T>::price(p.S[i], p.K[i], p.r[i], p.v[i], p.t[i]);
+  }
+};
+
+// splitmix64 (repro.py:21-30): draw i of stream `seed` mixes seed + (i+1)*golden.
+__device__ __forceinline__ u64 splitmix64_at(u64 seed, u64 i) {
+  u64 z = seed + (i + 1ull) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <class T> struct GenF {
+  struct Params {
+    T* out;
+    u64 seed, start;
+    int kind;
+    double a, b;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  struct Regs {};
+  static __device__ __forceinline__ T gen(const Params& p, i64 i) {
+    const u64 bits = splitmix64_at(p.seed, p.start + (u64)i);
+    if (p.kind == DRK_GEN_UNIFORM) {
+      // unit_doubles: (bits >> 11) * 2^-53, exact; uniform: lo + (hi - lo) * u (two roundings)
+      double u = (double)(bits >> 11) * 1.1102230246251565e-16;
+      if (!(p.a == 0.0 && p.b == 1.0)) u = __dadd_rn(p.a, __dmul_rn(__dsub_rn(p.b, p.a), u));
+      return (T)u;
+    }
+    const i64 m = (i64)(bits % (u64)p.a);
+    return (T)(m + (i64)p.b);
+  }
+  static __device__ __forceinline__ void load(const Params&, i64, Regs&) {}
+  static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs&) {
+    T a[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[e] = gen(p, i + e);
+    stv<T, E>(p.out + i, a);
+  }
+  static __device__ __forceinline__ void scalar(const Params& p, i64 i) { p.out[i] = gen(p, i); }
+};
+
+template <class F>
+static int launch_map(const typename F::Params& p, int64_t n, bool vec_ok, int device, void* stream,
+                      const char* what) {
+  if (n < 0) return set_error(DRK_E_ARG, std::string(what) + ": negative length");
+  if (n == 0) return 0;
+  if (int rc = prologue(device, what)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = sm_count(device);
+  if (vec_ok) {
+    auto k = map_vec_kernel<F, BLOCK, MAP_U>;
+    const int64_t nchunk = n / F::E;
+    int64_t grid = (nchunk + (int64_t)BLOCK * MAP_U - 1) / ((int64_t)BLOCK * MAP_U);
+    if (g_map_waves > 0) {
+      const int64_t cap = (int64_t)sms * occupancy(k, BLOCK, 0) * g_map_waves;
+      if (grid > cap) grid = cap;
+    }
+    // the scalar tail (n % E elements) is handled by the first threads of the grid
+    if (grid < 1) grid = 1;
+    if (grid > 0x7fffffff) grid = 0x7fffffff;
+    k<<<(unsigned)grid, BLOCK, 0, s>>>(p, n);
+  } else {
+    auto k = map_striped_kernel<F, BLOCK, MAP_U>;
+    int64_t grid = (n + (int64_t)BLOCK * MAP_U - 1) / ((int64_t)BLOCK * MAP_U);
+    const int64_t cap = (int64_t)sms * occupancy(k, BLOCK, 0) * 8;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    k<<<(unsigned)grid, BLOCK, 0, s>>>(p, n);
+  }
+  return epilogue(what);
+}
+
+#define DRK_DISPATCH(dtype, what, T, ...)                                         \
+  switch (dtype) {                                                               \
+    case DRK_F32: { typedef float T; __VA_ARGS__; }                              \
+    case DRK_F64: { typedef double T; __VA_ARGS__; }                             \
+    case DRK_I32: { typedef int T; __VA_ARGS__; }                                \
+    case DRK_I64: { typedef long long T; __VA_ARGS__; }                          \
+    default: return set_error(DRK_E_DTYPE, std::string(what) + ": unknown dtype"); \
+  }
+
+#define DRK_DISPATCH_FLOAT(dtype, what, T, ...)                                       \
+  switch (dtype) {                                                                   \
+    case DRK_F32: { typedef float T; __VA_ARGS__; }                                  \
+    case DRK_F64: { typedef double T; __VA_ARGS__; }                                 \
+    default: return set_error(DRK_E_DTYPE, std::string(what) + ": needs float32/float64"); \
+  }
+
+static int need(const void* p, const char* what, const char* arg) {
+  if (!p) return set_error(DRK_E_ARG, std::string(what) + ": null " + arg);
+  return 0;
+}
+
+extern "C" int drk_copy(int dtype, void* out, const void* in, int64_t n, int device, void* stream) {
+  if (n > 0 && (need(out, "drk_copy", "out") || need(in, "drk_copy", "in"))) return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_copy", T, {
+    typename CopyF<T>::Params p{(T*)out, (const T*)in};
+    return launch_map<CopyF<T>>(p, n, aligned16(out) && aligned16(in), device, stream, "drk_copy");
+  });
+}
+
+extern "C" int drk_fill(int dtype, void* out, int64_t n, const void* value, int device, void* stream) {
+  if (need(value, "drk_fill", "value")) return DRK_E_ARG;
+  if (n > 0 && need(out, "drk_fill", "out")) return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_fill", T, {
+    typename FillF<T>::Params p{(T*)out, *(const T*)value};
+    return launch_map<FillF<T>>(p, n, aligned16(out), device, stream, "drk_fill");
+  });
+}
+
+extern "C" int drk_iota(int dtype, void* out, int64_t n, int64_t start, int device, void* stream) {
+  if (n > 0 && need(out, "drk_iota", "out")) return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_iota", T, {
+    typename IotaF<T>::Params p{(T*)out, start};
+    return launch_map<IotaF<T>>(p, n, aligned16(out), device, stream, "drk_iota");
+  });
+}
+
+extern "C" int drk_scale(int dtype, void* out, const void* in, int64_t n, const void* alpha, int device,
+                         void* stream) {
+  if (need(alpha, "drk_scale", "alpha")) return DRK_E_ARG;
+  if (n > 0 && (need(out, "drk_scale", "out") || need(in, "drk_scale", "in"))) return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_scale", T, {
+    typename ScaleF<T>::Params p{(T*)out, (const T*)in, *(const T*)alpha};
+    return launch_map<ScaleF<T>>(p, n, aligned16(out) && aligned16(in), device, stream, "drk_scale");
+  });
+}
+
+extern "C" int drk_add(int dtype, void* out, const void* a, const void* b, int64_t n, int device,
+                       void* stream) {
+  if (n > 0 && (need(out, "drk_add", "out") || need(a, "drk_add", "a") || need(b, "drk_add", "b")))
+    return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_add", T, {
+    typename AddF<T>::Params p{(T*)out, (const T*)a, (const T*)b};
+    return launch_map<AddF<T>>(p, n, aligned16(out) && aligned16(a) && aligned16(b), device, stream,
+                               "drk_add");
+  });
+}
+
+extern "C" int drk_triad(int dtype, void* out, const void* b, const void* c, int64_t n, const void* alpha,
+                         int device, void* stream) {
+  if (need(alpha, "drk_triad", "alpha")) return DRK_E_ARG;
+  if (n > 0 && (need(out, "drk_triad", "out") || need(b, "drk_triad", "b") || need(c, "drk_triad", "c")))
+    return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_triad", T, {
+    typename TriadF<T>::Params p{(T*)out, (const T*)b, (const T*)c, *(const T*)alpha};
+    return launch_map<TriadF<T>>(p, n, aligned16(out) && aligned16(b) && aligned16(c), device, stream,
+                                 "drk_triad");
+  });
+}
+
+extern "C" int drk_black_scholes(int dtype, void* out, const void* S, const void* K, const void* r,
+                                 const void* v, const void* t, int64_t n, int device, void* stream) {
+  if (n > 0 && (need(out, "drk_black_scholes", "out") || need(S, "drk_black_scholes", "spot") ||
+                need(K, "drk_black_scholes", "strike") || need(r, "drk_black_scholes", "rate") ||
+                need(v, "drk_black_scholes", "volatility") || need(t, "drk_black_scholes", "expiry")))
+    return DRK_E_ARG;
+  DRK_DISPATCH_FLOAT(dtype, "drk_black_scholes", T, {
+    typename BlackScholesF<T>::Params p{(T*)out, (const T*)S, (const T*)K, (const T*)r, (const T*)v,
+                                        (const T*)t};
+    const bool al = aligned16(out) && aligned16(S) && aligned16(K) && aligned16(r) && aligned16(v) &&
+                    aligned16(t);
+    return launch_map<BlackScholesF<T>>(p, n, al, device, stream, "drk_black_scholes");
+  });
+}
+
+extern "C" int drk_generate(int dtype, void* out, int64_t n, uint64_t seed, uint64_t start, int kind,
+                            double a, double b, int device, void* stream) {
+  if (n > 0 && need(out, "drk_generate", "out")) return DRK_E_ARG;
+  if (kind != DRK_GEN_UNIFORM && kind != DRK_GEN_MOD)
+    return set_error(DRK_E_ARG, "drk_generate: unknown kind");
+  if (kind == DRK_GEN_MOD && !(a >= 1.0)) return set_error(DRK_E_ARG, "drk_generate: modulus must be >= 1");
+  DRK_DISPATCH(dtype, "drk_generate", T, {
+    typename GenF<T>::Params p{(T*)out, seed, start, kind, a, b};
+    return launch_map<GenF<T>>(p, n, aligned16(out), device, stream, "drk_generate");
+  });
+}
+
+// ---------------------------------------------------------------------------------------
+// reductions
+
+template <class T> struct IdentLoad {
+  typedef T V;
+  struct Params {
+    const T* x;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  static __device__ __forceinline__ void load(const Params& p, i64 i, T (&v)[E]) { ldv<T, E>(p.x + i, v); }
+  static __device__ __forceinline__ T one(const Params& p, i64 i) { return p.x[i]; }
+};
+
+// x[i] * y[i] rounded in T, as numpy's `t[0] * t[1]` temporary (bench.py:89).
+template <class T> struct ProdLoad {
+  typedef T V;
+  struct Params {
+    const T* x;
+    const T* y;
+  };
+  static constexpr int E = 16 / sizeof(T);
+  static __device__ __forceinline__ void load(const Params& p, i64 i, T (&v)[E]) {
+    T a[E], b[E];
+    ldv<T, E>(p.x + i, a);
+    ldv<T, E>(p.y + i, b);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = Arith<T>::mul(a[e], b[e]);
+  }
+  static __device__ __forceinline__ T one(const Params& p, i64 i) { return Arith<T>::mul(p.x[i], p.y[i]); }
+};
+
+extern "C" size_t drk_reduce_scratch_bytes(void) {
+  return 128 + (size_t)MAX_RED_GRID * (8 + 4);
+}
+
+static int acc_code(int dtype, int op) {
+  const bool widen = (op == DRK_ADD || op == DRK_MUL);
+  switch (dtype) {
+    case DRK_F32: return widen ? DRK_F64 : DRK_F32;
+    case DRK_F64: return DRK_F64;
+    case DRK_I32: return widen ? DRK_I64 : DRK_I32;
+    case DRK_I64: return DRK_I64;
+  }
+  return -1;
+}
+extern "C" int drk_acc_dtype(int dtype, int op) { return acc_code(dtype, op); }
+
+static ReduceScratch carve_reduce(void* scratch) {
+  ReduceScratch s;
+  char* b = (char*)scratch;
+  s.counter = (u32*)b;
+  s.partials = (void*)(b + 128);
+  s.has = (int*)(b + 128 + (size_t)MAX_RED_GRID * 8);
+  return s;
+}
+
+template <class LD, class Op>
+static int launch_reduce(const typename LD::Params& p, int64_t n, bool vec_ok, void* result, void* scratch,
+                         int device, void* stream, const char* what) {
+  typedef typename WideAcc<typename LD::V, Op>::type A;
+  if (n < 1) return set_error(DRK_E_ARG, std::string(what) + ": n must be >= 1");
+  if (!result || !scratch) return set_error(DRK_E_ARG, std::string(what) + ": null result/scratch");
+  if (int rc = prologue(device, what)) return rc;
+  auto k = reduce_kernel<LD, Op, BLOCK, RED_U>;
+  const int64_t work = vec_ok ? (n / LD::E) * 1 + 1 : n;
+  int64_t grid = (work + (int64_t)BLOCK * RED_U - 1) / ((int64_t)BLOCK * RED_U);
+  const int64_t cap = (int64_t)sm_count(device) * occupancy(k, BLOCK, 0) * (g_reduce_waves > 0 ? g_reduce_waves : 1);
+  if (grid > cap) grid = cap;
+  if (grid > MAX_RED_GRID) grid = MAX_RED_GRID;
+  if (grid < 1) grid = 1;
+  k<<<(unsigned)grid, BLOCK, 0, (cudaStream_t)stream>>>(p, n, vec_ok ? 1 : 0, carve_reduce(scratch), (A*)result,
+                                                       nullptr);
+  return epilogue(what);
+}
+
+template <class T>
+static int reduce_op(int op, const T* x, int64_t n, void* result, void* scratch, int device, void* stream) {
+  typename IdentLoad<T>::Params p{x};
+  const bool v = aligned16(x);
+  switch (op) {
+    case DRK_ADD: return launch_reduce<IdentLoad<T>, OpAdd>(p, n, v, result, scratch, device, stream, "drk_reduce");
+    case DRK_MUL: return launch_reduce<IdentLoad<T>, OpMul>(p, n, v, result, scratch, device, stream, "drk_reduce");
+    case DRK_MIN: return launch_reduce<IdentLoad<T>, OpMin>(p, n, v, result, scratch, device, stream, "drk_reduce");
+    case DRK_MAX: return launch_reduce<IdentLoad<T>, OpMax>(p, n, v, result, scratch, device, stream, "drk_reduce");
+  }
+  return set_error(DRK_E_ARG, "drk_reduce: unknown op");
+}
+
+extern "C" int drk_reduce(int dtype, int op, const void* x, int64_t n, void* result_dev, void* scratch,
+                          int device, void* stream) {
+  if (need(x, "drk_reduce", "x")) return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_reduce", T, { return reduce_op<T>(op, (const T*)x, n, result_dev, scratch, device, stream); });
+}
+
+extern "C" int drk_dot(int dtype, const void* x, const void* y, int64_t n, void* result_dev, void* scratch,
+                       int device, void* stream) {
+  if (need(x, "drk_dot", "x") || need(y, "drk_dot", "y")) return DRK_E_ARG;
+  DRK_DISPATCH(dtype, "drk_dot", T, {
+    typename ProdLoad<T>::Params p{(const T*)x, (const T*)y};
+    return launch_reduce<ProdLoad<T>, OpAdd>(p, n, aligned16(x) && aligned16(y), result_dev, scratch, device,
+                                             stream, "drk_dot");
+  });
+}
+
+// ---------------------------------------------------------------------------------------
+// scans
+
+template <class T, class Op> struct ScanItems {
+  // ITEMS * sizeof(T) / 16 odd => conflict-free 16-byte LDS of per-thread runs.
+  static constexpr int value =
+      sizeof(T) == 4 ? (sizeof(typename LocalAcc<T, Op>::type) == 4 ? 20 : 12) : 10;
+};
+
+template <class T, class Op> static size_t scan_scratch(int64_t n) {
+  typedef typename WideAcc<T, Op>::type A;
+  constexpr int TILE = BLOCK * ScanItems<T, Op>::value;
+  const size_t nt = (size_t)((n + TILE - 1) / TILE);
+  const size_t flags = ((nt * 4 + 127) / 128) * 128;
+  return 128 + flags + 2 * nt * sizeof(A) + 256;
+}
+
+template <class T, class Op>
+static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void* init_host, const void* carry_host,
+                       const void* carry_dev, void* seg_total, void* carry_out, void* scratch, size_t scratch_bytes,
+                       int device, void* stream) {
+  typedef typename WideAcc<T, Op>::type A;
+  constexpr int ITEMS = ScanItems<T, Op>::value;
+  typedef ScanConfig<T, T, Op, BLOCK, ITEMS> C;
+  const char* what = "drk_scan";
+  if (n < 1) return set_error(DRK_E_ARG, "drk_scan: n must be >= 1");
+  if (!in || !out) return set_error(DRK_E_ARG, "drk_scan: null in/out");
+  if (exclusive && !init_host) return set_error(DRK_E_ARG, "drk_scan: exclusive scan needs init");
+  if (carry_host && carry_dev) return set_error(DRK_E_ARG, "drk_scan: give at most one carry");
+  const size_t need_bytes = scan_scratch<T, Op>(n);
+  if (!scratch || scratch_bytes < need_bytes)
+    return set_error(DRK_E_SCRATCH, "drk_scan: scratch too small (need " + std::to_string(need_bytes) + ")");
+  const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
+  if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
+  if (int rc = prologue(device, what)) return rc;
+  const u32 nt = (u32)nt64;
+  char* b = (char*)scratch;
+  const size_t flags_bytes = ((nt * (size_t)4 + 127) / 128) * 128;
+  ScanParams<A, const T*> p;
+  memset(&p, 0, sizeof(p));
+  p.in = in;
+  p.out = out;
+  p.n = n;
+  p.ntiles = nt;
+  p.exclusive = exclusive;
+  p.has_init = init_host != nullptr;
+  if (init_host) memcpy(&p.init, init_host, sizeof(A));
+  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
+  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
+  p.carry_ptr = (const A*)carry_dev;
+  p.seg_total = (A*)seg_total;
+  p.carry_out = (A*)carry_out;
+  p.counter = (u32*)b;
+  p.flags = (u32*)(b + 128);
+  p.aggs = (A*)(b + 128 + flags_bytes);
+  p.incls = p.aggs + nt;
+  p.bulk_ok = aligned16(in) && aligned16(out);
+  cudaStream_t s = (cudaStream_t)stream;
+  DRK_CHECK(cudaMemsetAsync(b, 0, 128 + flags_bytes, s));
+  auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS>;
+  k<<<nt, BLOCK, C::SMEM, s>>>(p);
+  return epilogue(what);
+}
+
+template <class T>
+static int scan_op(int op, int exclusive, const T* in, T* out, int64_t n, const void* init_host,
+                   const void* carry_host, const void* carry_dev, void* seg_total, void* carry_out, void* scratch,
+                   size_t sb, int device, void* stream) {
+  switch (op) {
+    case DRK_ADD:
+      return launch_scan<T, OpAdd>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
+                                   scratch, sb, device, stream);
+    case DRK_MUL:
+      return launch_scan<T, OpMul>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
+                                   scratch, sb, device, stream);
+    case DRK_MIN:
+      return launch_scan<T, OpMin>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
+                                   scratch, sb, device, stream);
+    case DRK_MAX:
+      return launch_scan<T, OpMax>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
+                                   scratch, sb, device, stream);
+  }
+  return set_error(DRK_E_ARG, "drk_scan: unknown op");
+}
+
+extern "C" size_t drk_scan_scratch_bytes(int dtype, int op, int64_t n) {
+  if (n < 1) n = 1;
+#define DRK_SS(T)                                               \
+  switch (op) {                                                 \
+    case DRK_ADD: return scan_scratch<T, OpAdd>(n);             \
+    case DRK_MUL: return scan_scratch<T, OpMul>(n);             \
+    case DRK_MIN: return scan_scratch<T, OpMin>(n);             \
+    case DRK_MAX: return scan_scratch<T, OpMax>(n);             \
+    default: return 0;                                          \
+  }
+  switch (dtype) {
+    case DRK_F32: DRK_SS(float)
+    case DRK_F64: DRK_SS(double)
+    case DRK_I32: DRK_SS(int)
+    case DRK_I64: DRK_SS(long long)
+  }
+#undef DRK_SS
+  return 0;
+}
+
+extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_t n,
+                        const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total_dev,
+                        void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream) {
+  DRK_DISPATCH(dtype, "drk_scan", T, {
+    return scan_op<T>(op, exclusive, (const T*)in, (T*)out, n, init_host, carry_host, carry_dev, seg_total_dev,
+                      carry_out_dev, scratch, scratch_bytes, device, stream);
+  });
+}

@@ -1,0 +1,273 @@
+"""Lowered segment work -> libdrk launches.
+
+Each algorithm hands this module per-segment work already lowered by views.py: a list
+of leaves (device buffers, index ranges, host slices) and an expression over them.  The
+expression is first matched against the ahead-of-time catalogue of hand-written sm_100a
+kernels in libdrk.so — copy, fill, iota, scale, add, triad, Black-Scholes, reduce,
+dot, scan — which cover the benchmarked paths (bench.py:87-126 of the reference).  Any
+other expression is compiled once by NVRTC from generated CUDA (codegen.py) and cached.
+There is no host evaluation path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib, expr
+from .views import Leaf, Target
+
+OPCODES = {"add": _lib.ADD, "multiply": _lib.MUL, "minimum": _lib.MIN, "maximum": _lib.MAX}
+
+# Optional live kernel timing: when enabled, every launch is bracketed by CUDA events on
+# the stream it is launched on (bench.py uses this inside its timed region).
+_PROFILE = None
+
+
+class profile:
+    """Context manager collecting {kernel name: [(start_event, end_event, elements)]}."""
+
+    def __enter__(self):
+        global _PROFILE
+        self.records = {}
+        _PROFILE = self.records
+        return self
+
+    def __exit__(self, *exc):
+        global _PROFILE
+        _PROFILE = None
+        return False
+
+    def summary(self):
+        """{name: (launches, total_ms, total_elements)} — call after synchronising."""
+        out = {}
+        for name, recs in self.records.items():
+            ms = sum(s.elapsed_time(e) for s, e, _ in recs)
+            out[name] = (len(recs), ms, sum(n for _, _, n in recs))
+        return out
+
+
+def launch_kernel(name, launch_ctx, n, *args):
+    """Call libdrk entry `name` (device and stream appended) on launch_ctx."""
+    if _PROFILE is None:
+        _lib.call(name, *args, launch_ctx.device, launch_ctx.stream)
+        return
+    from .runtime import torch
+
+    t = torch()
+    s, e = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    s.record(launch_ctx.state.stream)
+    _lib.call(name, *args, launch_ctx.device, launch_ctx.stream)
+    e.record(launch_ctx.state.stream)
+    _PROFILE.setdefault(name, []).append((s, e, n))
+
+
+class Launch:
+    """Execution context of one segment: device, stream, device state, keep-alive list."""
+
+    __slots__ = ("state", "device", "stream", "keep")
+
+    def __init__(self, state):
+        self.state = state
+        self.device = state.index
+        self.stream = state.handle
+        self.keep = []
+
+
+def stage_leaves(leaves, launch: Launch):
+    """Make every leaf readable by a kernel on launch.device: host slices are copied to
+    the device (asynchronously, on the segment stream).  Returns per-leaf pointers (0 for
+    index leaves)."""
+    ptrs = []
+    for lf in leaves:
+        if lf.kind == "array":
+            ptrs.append(lf.ptr())
+        elif lf.kind == "host":
+            from .runtime import torch
+
+            t = torch()
+            arr = np.ascontiguousarray(lf.host)
+            with t.cuda.stream(launch.state.stream):
+                dev = t.from_numpy(arr).to(launch.state.device, non_blocking=False)
+            launch.keep.append(dev)
+            ptrs.append(dev.data_ptr())
+        else:
+            ptrs.append(0)
+    return ptrs
+
+
+def _is_leaf(node, leaves, kind="array"):
+    return node.op == "leaf" and leaves[node.value].kind == kind
+
+
+def _uniform(node, dtype):
+    """All loop dtypes of node equal dtype."""
+    return node.loop is not None and all(d == dtype for d in node.loop)
+
+
+def _scalar_arg(value, dtype):
+    return _lib.scalar_buffer(value, dtype)
+
+
+# ----------------------------------------------------------------------------------------
+# map
+
+
+def match_map(node, leaves, out_dtype):
+    """Catalogue entry for `out <- node` or None.  Returns (fn_name, arg_builder)."""
+    T = np.dtype(out_dtype)
+    if T not in _lib.DTYPE_CODE:
+        return None
+    code = _lib.DTYPE_CODE[T]
+    if node.op == "const":
+        return ("drk_fill", lambda out, n, ptrs, L: (code, out, n, _keep(L, _scalar_arg(node.value, T))))
+    if node.op == "leaf":
+        lf = leaves[node.value]
+        if lf.kind == "index":
+            return ("drk_iota", lambda out, n, ptrs, L: (code, out, n, lf.base))
+        if lf.dtype == T:
+            k = node.value
+            return ("drk_copy", lambda out, n, ptrs, L: (code, out, ptrs[k], n))
+        return None
+    if node.dtype != T:
+        return None
+    if node.op == "multiply" and _uniform(node, T):
+        a, b = node.args
+        if a.op == "const" and _is_leaf(b, leaves):
+            a, b = b, a
+        if b.op == "const" and _is_leaf(a, leaves):
+            k, alpha = a.value, b.value
+            return ("drk_scale", lambda out, n, ptrs, L: (code, out, ptrs[k], n, _keep(L, _scalar_arg(alpha, T))))
+    if node.op == "add" and _uniform(node, T):
+        a, b = node.args
+        if _is_leaf(a, leaves) and _is_leaf(b, leaves):
+            ka, kb = a.value, b.value
+            return ("drk_add", lambda out, n, ptrs, L: (code, out, ptrs[ka], ptrs[kb], n))
+        # b + alpha*c (either operand order; IEEE add and multiply commute bit-exactly)
+        for x, y in ((a, b), (b, a)):
+            if _is_leaf(x, leaves) and y.op == "multiply" and _uniform(y, T):
+                p, q = y.args
+                if p.op == "const" and _is_leaf(q, leaves):
+                    p, q = q, p
+                if q.op == "const" and _is_leaf(p, leaves):
+                    kb, kc, alpha = x.value, p.value, q.value
+                    return ("drk_triad", lambda out, n, ptrs, L: (
+                        code, out, ptrs[kb], ptrs[kc], n, _keep(L, _scalar_arg(alpha, T))))
+    if node.op == "call:black_scholes" and T.kind == "f" and all(_is_leaf(a, leaves) and a.dtype == T
+                                                                 for a in node.args):
+        ks = [a.value for a in node.args]
+        return ("drk_black_scholes", lambda out, n, ptrs, L: (code, out, *[ptrs[k] for k in ks], n))
+    return None
+
+
+def _keep(launch, buf):
+    launch.keep.append(buf)
+    return buf
+
+
+def run_map(writes, leaves, n, launch: Launch):
+    """Write each (Target, node) of `writes` for n elements on launch's device."""
+    if n == 0 or not writes:
+        return
+    leaves = _dealias(writes, leaves, n, launch)
+    ptrs = stage_leaves(leaves, launch)
+    if len(writes) == 1:
+        tgt, node = writes[0]
+        m = match_map(node, leaves, tgt.dtype)
+        if m is not None:
+            name, build = m
+            launch_kernel(name, launch, n, *build(tgt.ptr(), n, ptrs, launch))
+            return
+    from . import codegen
+
+    codegen.run_map(writes, leaves, ptrs, n, launch)
+
+
+def _dealias(writes, leaves, n, launch):
+    """Leaves that overlap a written range at a different offset are snapshotted first
+    (the reference computes the whole right-hand side before storing, views.py:176)."""
+    out = list(leaves)
+    for i, lf in enumerate(leaves):
+        if lf.kind != "array":
+            continue
+        for tgt, _ in writes:
+            if lf.handle is tgt.handle and lf.start != tgt.start:
+                lo, hi = lf.start, lf.start + n
+                if lo < tgt.start + n and tgt.start < hi:
+                    from .runtime import torch
+
+                    t = torch()
+                    with t.cuda.stream(launch.state.stream):
+                        snap = t.empty(n, dtype=lf.handle.span().dtype, device=launch.state.device)
+                    _lib.call("drk_memcpy_async", snap.data_ptr(), lf.ptr(), n * lf.dtype.itemsize,
+                              launch.device, launch.stream)
+                    launch.keep.append(snap)
+                    out[i] = _TensorLeaf(snap, lf.dtype, n)
+                    break
+    return out
+
+
+class _TensorLeaf(Leaf):
+    __slots__ = ("tensor",)
+
+    def __init__(self, tensor, dtype, n):
+        super().__init__("array", n, dtype)
+        self.tensor = tensor
+
+    def ptr(self):
+        return self.tensor.data_ptr()
+
+
+# ----------------------------------------------------------------------------------------
+# reduce
+
+
+def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
+    """Reduce `node` over n elements into result slot `slot` of launch.state (value in
+    drk_acc_dtype(node.dtype, op) for catalogue ops)."""
+    ptrs = stage_leaves(leaves, launch)
+    st = launch.state
+    res = st.result_dev_ptr(slot)
+    T = node.dtype
+    if opcode is not None and T in _lib.DTYPE_CODE:
+        code = _lib.DTYPE_CODE[T]
+        if node.op == "leaf" and leaves[node.value].kind == "array":
+            launch_kernel("drk_reduce", launch, n, code, opcode, ptrs[node.value], n, res,
+                                st.reduce_scratch.data_ptr())
+            return
+        if (opcode == _lib.ADD and node.op == "multiply" and _uniform(node, T)
+                and all(_is_leaf(a, leaves) for a in node.args)):
+            a, b = node.args
+            launch_kernel("drk_dot", launch, n, code, ptrs[a.value], ptrs[b.value], n, res,
+                                st.reduce_scratch.data_ptr())
+            return
+    from . import codegen
+
+    codegen.run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot)
+
+
+# ----------------------------------------------------------------------------------------
+# scan
+
+
+def run_scan(dtype, opcode, exclusive, in_ptr, out_ptr, n, lctx: Launch, *, init=None, carry_value=None,
+             carry_dev=None, seg_total_slot=None, carry_out_slot=None):
+    """One drk_scan over a plain device buffer (the caller materialises views first)."""
+    T = np.dtype(dtype)
+    code = _lib.dtype_code(T)
+    A = _lib.acc_dtype(T, opcode)
+    st = lctx.state
+    nbytes = int(_lib.load().drk_scan_scratch_bytes(code, opcode, n))
+    scratch = st.scan_scratch(nbytes)
+    init_buf = _keep(lctx, _scalar_arg(init, A)) if init is not None else None
+    carry_buf = _keep(lctx, _scalar_arg(carry_value, A)) if carry_value is not None else None
+    launch_kernel(
+        "drk_scan", lctx, n, code, opcode, 1 if exclusive else 0, in_ptr, out_ptr, n,
+        ctypes.addressof(init_buf) if init_buf is not None else None,
+        ctypes.addressof(carry_buf) if carry_buf is not None else None,
+        carry_dev,
+        st.result_dev_ptr(seg_total_slot) if seg_total_slot is not None else None,
+        st.result_dev_ptr(carry_out_slot) if carry_out_slot is not None else None,
+        scratch.data_ptr(), scratch.numel(),
+    )
