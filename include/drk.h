@@ -104,7 +104,9 @@ int drk_dot(int dtype, const void* x, const void* y, int64_t n, void* result_dev
  *   carry_out_dev out: carry ⊕ segment total (A), or NULL
  * inclusive: out[j] = carry ⊕ in[0..j];  exclusive: out[0] = init ⊕ carry,
  * out[j] = init ⊕ carry ⊕ in[0..j-1].  in == out (in place) is allowed.  n >= 1.
- * `scratch` must hold drk_scan_scratch_bytes(dtype, op, n) bytes (no initialisation). */
+ * `scratch` must hold drk_scan_scratch_bytes(dtype, op, n) bytes, be zero-filled once when
+ * allocated, and be used only by drk_scan calls on one stream (tile descriptors are
+ * epoch-tagged per call, so nothing is cleared between calls). */
 size_t drk_scan_scratch_bytes(int dtype, int op, int64_t n);
 int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_t n,
              const void* init_host, const void* carry_host, const void* carry_dev,

@@ -632,11 +632,16 @@ template <class T, class Op> struct ScanItems {
 };
 
 template <class T, class Op> static size_t scan_scratch(int64_t n) {
-  typedef typename WideAcc<T, Op>::type A;
   constexpr int TILE = BLOCK * ScanItems<T, Op>::value;
   const size_t nt = (size_t)((n + TILE - 1) / TILE);
-  const size_t flags = ((nt * 4 + 127) / 128) * 128;
-  return 128 + flags + 2 * nt * sizeof(A) + 256;
+  return 128 + nt * 16;
+}
+
+// Per-scratch launch epochs (tile descriptors of older launches then read as stale).
+static std::unordered_map<uintptr_t, uint64_t> g_scan_epochs;
+static uint64_t next_epoch(void* scratch) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return ++g_scan_epochs[(uintptr_t)scratch];
 }
 
 template <class T, class Op>
@@ -659,7 +664,6 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   if (int rc = prologue(device, what)) return rc;
   const u32 nt = (u32)nt64;
   char* b = (char*)scratch;
-  const size_t flags_bytes = ((nt * (size_t)4 + 127) / 128) * 128;
   ScanParams<A, const T*> p;
   memset(&p, 0, sizeof(p));
   p.in = in;
@@ -675,12 +679,10 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   p.seg_total = (A*)seg_total;
   p.carry_out = (A*)carry_out;
   p.counter = (u32*)b;
-  p.flags = (u32*)(b + 128);
-  p.aggs = (A*)(b + 128 + flags_bytes);
-  p.incls = p.aggs + nt;
+  p.desc = (u64*)(b + 128);
+  p.epoch = next_epoch(scratch);
   p.bulk_ok = aligned16(in) && aligned16(out);
   cudaStream_t s = (cudaStream_t)stream;
-  DRK_CHECK(cudaMemsetAsync(b, 0, 128 + flags_bytes, s));
   auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS>;
   k<<<nt, BLOCK, C::SMEM, s>>>(p);
   return epilogue(what);

@@ -120,7 +120,8 @@ class DeviceState:
         t = torch()
         if self._scan_scratch is None or self._scan_scratch.numel() < nbytes:
             with t.cuda.stream(self.stream):
-                self._scan_scratch = t.empty(int(nbytes * 1.25) + 4096, dtype=t.uint8, device=self.device)
+                # zero once: tile descriptors are epoch-tagged, the ticket counter self-resets
+                self._scan_scratch = t.zeros(int(nbytes * 1.25) + 4096, dtype=t.uint8, device=self.device)
         return self._scan_scratch
 
     def ensure_results(self, slots: int):
