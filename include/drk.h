@@ -116,6 +116,9 @@ int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_
 /* ---- tuning / introspection ------------------------------------------------------------ */
 /* set a launch parameter by name ("map_waves", "reduce_waves"); returns the old value */
 int drk_tune(const char* name, int value);
+/* debug: when non-null, scans record 8 uint64 per tile (%globaltimer stamps: ticket, data
+ * ready, aggregate published, look-back done, outputs staged, end; look-back rounds; SM) */
+int drk_scan_set_trace(void* buffer);
 /* number of kernels this library has launched in this process */
 int64_t drk_launch_count(void);
 

@@ -77,6 +77,7 @@ SIGNATURES = {
     "drk_scan_scratch_bytes": (_sz, [_int, _int, _i64]),
     "drk_scan": (_int, [_int, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "drk_tune": (_int, [_cp, _int]),
+    "drk_scan_set_trace": (_int, [_vp]),
     "drk_launch_count": (_i64, []),
     "drk_note_launch": (_i64, []),
     "drk_jit_compile": (_int, [_cp, _cp, _cp, ctypes.POINTER(_vp), ctypes.c_char_p, _sz]),

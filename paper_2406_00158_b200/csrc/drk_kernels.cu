@@ -106,6 +106,16 @@ static constexpr int MAX_RED_GRID = 4096;
 static std::mutex g_mu;
 static int g_map_waves = 0;     // 0: size grid to cover the work once (non-persistent)
 static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
+static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
+static int g_scan_static = 0;    // persistent static-schedule scan (cooperative launch)
+static int g_scan_l2 = 1;        // L2-resident two-touch scan for large segments
+static int g_scan_l2_min = 1 << 22;
+static int g_scan_ctas = 0;      // CTAs per SM of the static scan (0: occupancy)
+static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
+extern "C" int drk_scan_set_trace(void* buf) {
+  g_scan_trace = buf;
+  return 0;
+}
 
 extern "C" int drk_tune(const char* name, int value) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -117,6 +127,21 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "reduce_waves")) {
     old = g_reduce_waves;
     g_reduce_waves = value;
+  } else if (!strcmp(name, "scan_l2")) {
+    old = g_scan_l2;
+    g_scan_l2 = value;
+  } else if (!strcmp(name, "scan_l2_min")) {
+    old = g_scan_l2_min;
+    g_scan_l2_min = value;
+  } else if (!strcmp(name, "scan_static")) {
+    old = g_scan_static;
+    g_scan_static = value;
+  } else if (!strcmp(name, "scan_ctas")) {
+    old = g_scan_ctas;
+    g_scan_ctas = value;
+  } else if (!strcmp(name, "scan_sub")) {
+    old = g_scan_sub;
+    if (value >= 1 && value <= 4) g_scan_sub = value;
   }
   return old;
 }
@@ -630,8 +655,10 @@ template <class T, class Op> struct ScanItems {
   static constexpr int value =
       sizeof(T) == 4 ? (sizeof(typename LocalAcc<T, Op>::type) == 4 ? 20 : 12) : 10;
 };
+static constexpr int SCAN_SUB_MAX = 4;
 
 template <class T, class Op> static size_t scan_scratch(int64_t n) {
+  // sized for the smallest tile (SUB = 1) so any g_scan_sub fits
   constexpr int TILE = BLOCK * ScanItems<T, Op>::value;
   const size_t nt = (size_t)((n + TILE - 1) / TILE);
   return 128 + nt * 16;
@@ -644,13 +671,65 @@ static uint64_t next_epoch(void* scratch) {
   return ++g_scan_epochs[(uintptr_t)scratch];
 }
 
+template <class T, class Op, int SUB>
+static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+  constexpr int ITEMS = ScanItems<T, Op>::value;
+  typedef ScanConfig<T, T, Op, BLOCK, ITEMS, SUB> C;
+  const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
+  if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
+  p.ntiles = (u32)nt64;
+  if (p.bulk_ok && g_scan_l2 && n >= (int64_t)g_scan_l2_min) {
+    constexpr int ITEMS = ScanItems<T, Op>::value;
+    constexpr int SUBS = 6;
+    constexpr int TILE = BLOCK * ITEMS * SUBS;
+    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS>;
+    const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
+    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int dev = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
+    if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
+    const int64_t nt = (n + TILE - 1) / TILE;
+    auto p2 = p;
+    p2.ntiles = (u32)nt;
+    int64_t grid = (int64_t)sm_count(dev) * per_sm;
+    if (grid > nt) grid = nt;
+    if (per_sm >= 1) {
+      void* args[] = {(void*)&p2};
+      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
+      if (e == cudaSuccess) return 0;
+      cudaGetLastError();
+    }
+  }
+  if (p.bulk_ok && g_scan_static) {
+    constexpr int NS = 4, PF = 2;
+    auto k = scan_static_kernel<T, Op, BLOCK, ITEMS, SUB, NS, PF>;
+    const int smem = NS * C::IN_BYTES;
+    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int dev = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
+    if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
+    int64_t grid = (int64_t)sm_count(dev) * per_sm;
+    if (grid > (int64_t)p.ntiles) grid = p.ntiles;
+    if (per_sm >= 1) {
+      void* args[] = {(void*)&p};
+      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
+      if (e == cudaSuccess) return 0;
+      cudaGetLastError();  // fall through to the one-tile-per-CTA kernel
+    }
+  }
+  auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS, SUB>;
+  if (C::SMEM > 48 * 1024) DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  k<<<p.ntiles, BLOCK, C::SMEM, s>>>(p);
+  return 0;
+}
+
 template <class T, class Op>
 static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void* init_host, const void* carry_host,
                        const void* carry_dev, void* seg_total, void* carry_out, void* scratch, size_t scratch_bytes,
                        int device, void* stream) {
   typedef typename WideAcc<T, Op>::type A;
-  constexpr int ITEMS = ScanItems<T, Op>::value;
-  typedef ScanConfig<T, T, Op, BLOCK, ITEMS> C;
   const char* what = "drk_scan";
   if (n < 1) return set_error(DRK_E_ARG, "drk_scan: n must be >= 1");
   if (!in || !out) return set_error(DRK_E_ARG, "drk_scan: null in/out");
@@ -659,17 +738,13 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   const size_t need_bytes = scan_scratch<T, Op>(n);
   if (!scratch || scratch_bytes < need_bytes)
     return set_error(DRK_E_SCRATCH, "drk_scan: scratch too small (need " + std::to_string(need_bytes) + ")");
-  const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
-  if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
   if (int rc = prologue(device, what)) return rc;
-  const u32 nt = (u32)nt64;
   char* b = (char*)scratch;
   ScanParams<A, const T*> p;
   memset(&p, 0, sizeof(p));
   p.in = in;
   p.out = out;
   p.n = n;
-  p.ntiles = nt;
   p.exclusive = exclusive;
   p.has_init = init_host != nullptr;
   if (init_host) memcpy(&p.init, init_host, sizeof(A));
@@ -682,9 +757,16 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   p.desc = (u64*)(b + 128);
   p.epoch = next_epoch(scratch);
   p.bulk_ok = aligned16(in) && aligned16(out);
+  p.trace = (u64*)g_scan_trace;
   cudaStream_t s = (cudaStream_t)stream;
-  auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS>;
-  k<<<nt, BLOCK, C::SMEM, s>>>(p);
+  int rc = 0;
+  switch (g_scan_sub) {
+    case 1: rc = launch_scan_sub<T, Op, 1>(p, n, s); break;
+    case 3: rc = launch_scan_sub<T, Op, 3>(p, n, s); break;
+    case 4: rc = launch_scan_sub<T, Op, 4>(p, n, s); break;
+    default: rc = launch_scan_sub<T, Op, 2>(p, n, s); break;
+  }
+  if (rc) return rc;
   return epilogue(what);
 }
 

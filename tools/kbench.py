@@ -36,6 +36,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--log2n", type=int, default=30)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--tune", default="", help="name=value,... passed to drk_tune")
     ap.add_argument("--only", default="copy,triad,dot,reduce,scan_f32,scan_i32,scan_f64,scan_excl_i32,bs")
     args = ap.parse_args()
     n = 1 << args.log2n
@@ -44,6 +45,9 @@ def main():
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     lib = _lib.load()
+    for kv in filter(None, args.tune.split(",")):
+        k, v = kv.split("=")
+        lib.drk_tune(k.encode(), int(v))
     a = torch.empty(n, dtype=torch.float32, device=dev)
     b = torch.rand(n, dtype=torch.float32, device=dev)
     c = torch.rand(n, dtype=torch.float32, device=dev)
