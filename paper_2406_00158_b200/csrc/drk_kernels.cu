@@ -110,6 +110,10 @@ static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
 static int g_scan_static = 0;    // persistent static-schedule scan (cooperative launch)
 static int g_scan_l2 = 1;        // L2-resident two-touch scan for large segments
 static int g_scan_l2_min = 1 << 22;
+static int g_scan_l2_subs = 6;
+static int g_scan_ahead = 0;     // read-ahead persistent scan
+static int g_scan_l2dyn = 1;     // L2 two-touch, one ticketed tile per CTA
+static int g_scan_ahead_subs = 2;
 static int g_scan_ctas = 0;      // CTAs per SM of the static scan (0: occupancy)
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
 extern "C" int drk_scan_set_trace(void* buf) {
@@ -130,6 +134,18 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2")) {
     old = g_scan_l2;
     g_scan_l2 = value;
+  } else if (!strcmp(name, "scan_l2dyn")) {
+    old = g_scan_l2dyn;
+    g_scan_l2dyn = value;
+  } else if (!strcmp(name, "scan_ahead")) {
+    old = g_scan_ahead;
+    g_scan_ahead = value;
+  } else if (!strcmp(name, "scan_ahead_subs")) {
+    old = g_scan_ahead_subs;
+    g_scan_ahead_subs = value;
+  } else if (!strcmp(name, "scan_l2_subs")) {
+    old = g_scan_l2_subs;
+    g_scan_l2_subs = value;
   } else if (!strcmp(name, "scan_l2_min")) {
     old = g_scan_l2_min;
     g_scan_l2_min = value;
@@ -671,6 +687,69 @@ static uint64_t next_epoch(void* scratch) {
   return ++g_scan_epochs[(uintptr_t)scratch];
 }
 
+template <class T, class Op, int SUBS>
+static int launch_scan_ahead(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+  constexpr int ITEMS = ScanItems<T, Op>::value;
+  constexpr int TILE = BLOCK * ITEMS * SUBS;
+  auto k = scan_ahead_kernel<T, Op, BLOCK, ITEMS, SUBS>;
+  const int smem = 2 * TILE * (int)sizeof(T);
+  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
+  if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
+  if (per_sm < 1) return -1;
+  const int64_t nt = (n + TILE - 1) / TILE;
+  auto p2 = p;
+  p2.ntiles = (u32)nt;
+  int64_t grid = (int64_t)sm_count(dev) * per_sm;
+  if (grid > nt) grid = nt;
+  void* args[] = {(void*)&p2};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
+  if (e == cudaSuccess) return 0;
+  cudaGetLastError();
+  return -1;
+}
+
+template <class T, class Op, int SUBS>
+static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+  constexpr int ITEMS = ScanItems<T, Op>::value;
+  constexpr int TILE = BLOCK * ITEMS * SUBS;
+  auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, true>;
+  const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
+  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int64_t nt = (n + TILE - 1) / TILE;
+  auto p2 = p;
+  p2.ntiles = (u32)nt;
+  k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
+  return 0;
+}
+
+// Returns 0 on launch, an error code, or -1 when the cooperative launch is not possible.
+template <class T, class Op, int SUBS>
+static int launch_scan_l2(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+  constexpr int ITEMS = ScanItems<T, Op>::value;
+  constexpr int TILE = BLOCK * ITEMS * SUBS;
+  auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS>;
+  const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
+  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int dev = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
+  if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
+  if (per_sm < 1) return -1;
+  const int64_t nt = (n + TILE - 1) / TILE;
+  auto p2 = p;
+  p2.ntiles = (u32)nt;
+  int64_t grid = (int64_t)sm_count(dev) * per_sm;
+  if (grid > nt) grid = nt;
+  void* args[] = {(void*)&p2};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
+  if (e == cudaSuccess) return 0;
+  cudaGetLastError();
+  return -1;
+}
+
 template <class T, class Op, int SUB>
 static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int ITEMS = ScanItems<T, Op>::value;
@@ -678,28 +757,35 @@ static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& 
   const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
   if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
   p.ntiles = (u32)nt64;
-  if (p.bulk_ok && g_scan_l2 && n >= (int64_t)g_scan_l2_min) {
-    constexpr int ITEMS = ScanItems<T, Op>::value;
-    constexpr int SUBS = 6;
-    constexpr int TILE = BLOCK * ITEMS * SUBS;
-    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS>;
-    const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
-    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int dev = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
-    if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
-    const int64_t nt = (n + TILE - 1) / TILE;
-    auto p2 = p;
-    p2.ntiles = (u32)nt;
-    int64_t grid = (int64_t)sm_count(dev) * per_sm;
-    if (grid > nt) grid = nt;
-    if (per_sm >= 1) {
-      void* args[] = {(void*)&p2};
-      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
-      if (e == cudaSuccess) return 0;
-      cudaGetLastError();
+  if (p.bulk_ok && g_scan_l2dyn && n >= (int64_t)g_scan_l2_min) {
+    switch (g_scan_l2_subs) {
+      case 2: return launch_scan_l2dyn<T, Op, 2>(p, n, s);
+      case 4: return launch_scan_l2dyn<T, Op, 4>(p, n, s);
+      case 8: return launch_scan_l2dyn<T, Op, 8>(p, n, s);
+      case 12: return launch_scan_l2dyn<T, Op, 12>(p, n, s);
+      case 16: return launch_scan_l2dyn<T, Op, 16>(p, n, s);
+      default: return launch_scan_l2dyn<T, Op, 6>(p, n, s);
     }
+  }
+  if (p.bulk_ok && g_scan_ahead && n >= (int64_t)g_scan_l2_min) {
+    int rc = -1;
+    switch (g_scan_ahead_subs) {
+      case 1: rc = launch_scan_ahead<T, Op, 1>(p, n, s); break;
+      case 3: rc = launch_scan_ahead<T, Op, 3>(p, n, s); break;
+      case 4: rc = launch_scan_ahead<T, Op, 4>(p, n, s); break;
+      default: rc = launch_scan_ahead<T, Op, 2>(p, n, s); break;
+    }
+    if (rc >= 0) return rc;
+  }
+  if (p.bulk_ok && g_scan_l2 && n >= (int64_t)g_scan_l2_min) {
+    int rc = -1;
+    switch (g_scan_l2_subs) {
+      case 2: rc = launch_scan_l2<T, Op, 2>(p, n, s); break;
+      case 4: rc = launch_scan_l2<T, Op, 4>(p, n, s); break;
+      case 8: rc = launch_scan_l2<T, Op, 8>(p, n, s); break;
+      default: rc = launch_scan_l2<T, Op, 6>(p, n, s); break;
+    }
+    if (rc >= 0) return rc;
   }
   if (p.bulk_ok && g_scan_static) {
     constexpr int NS = 4, PF = 2;
