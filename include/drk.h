@@ -138,6 +138,18 @@ int drk_jit_launch(void* handle, const char* kernel, unsigned grid, unsigned blo
 int drk_jit_occupancy(void* handle, const char* kernel, unsigned block, unsigned smem,
                       int device, int* blocks_per_sm, int* sm_count);
 
+/* scan with an NVRTC-compiled scan kernel (a custom associative operator): the kernel
+ * `kernel` of module `handle` must be a scan_kernel instantiation over a plain input with
+ * accumulator size acc_bytes (4 or 8), tile = elements per CTA, smem_bytes = its dynamic
+ * shared memory.  Other arguments as drk_scan; scratch of drk_jit_scan_scratch_bytes(). */
+size_t drk_jit_scan_scratch_bytes(int64_t n, int tile);
+int drk_jit_scan(void* handle, const char* kernel, int acc_bytes, int tile, int smem_bytes, int exclusive,
+                 const void* in, void* out, int64_t n, const void* init_host, const void* carry_host,
+                 const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
+                 size_t scratch_bytes, int device, void* stream);
+const char* drk_jit_last_error(void);
+int64_t drk_note_launch(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,9 @@ SIGNATURES = {
     "drk_jit_occupancy": (_int, [_vp, _cp, ctypes.c_uint, ctypes.c_uint, _int,
                                  ctypes.POINTER(_int), ctypes.POINTER(_int)]),
     "drk_jit_last_error": (_cp, []),
+    "drk_jit_scan_scratch_bytes": (_sz, [_i64, _int]),
+    "drk_jit_scan": (_int, [_vp, _cp, _int, _int, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                            _int, _vp]),
 }
 
 _lock = threading.Lock()
@@ -129,8 +132,10 @@ def last_error() -> str:
 def check(rc: int, func: str) -> None:
     if rc != 0:
         lib = load()
-        msg = lib.drk_jit_last_error() if func.startswith("drk_jit") else lib.drk_last_error()
-        raise DrkError(rc, func, msg.decode(errors="replace") if msg else "")
+        msg = lib.drk_last_error() or b""
+        if func.startswith("drk_jit"):
+            msg = (lib.drk_jit_last_error() or b"") or msg
+        raise DrkError(rc, func, msg.decode(errors="replace"))
 
 
 def call(name: str, *args) -> None:

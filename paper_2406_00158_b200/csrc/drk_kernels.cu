@@ -107,14 +107,9 @@ static std::mutex g_mu;
 static int g_map_waves = 0;     // 0: size grid to cover the work once (non-persistent)
 static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
 static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
-static int g_scan_static = 0;    // persistent static-schedule scan (cooperative launch)
-static int g_scan_l2 = 1;        // L2-resident two-touch scan for large segments
+static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned segments
 static int g_scan_l2_min = 1 << 22;
-static int g_scan_l2_subs = 6;
-static int g_scan_ahead = 0;     // read-ahead persistent scan
-static int g_scan_l2dyn = 1;     // L2 two-touch, one ticketed tile per CTA
-static int g_scan_ahead_subs = 2;
-static int g_scan_ctas = 0;      // CTAs per SM of the static scan (0: occupancy)
+static int g_scan_l2_subs = 6;   // sub-tiles per L2 tile (120 KB for fp32)
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
 extern "C" int drk_scan_set_trace(void* buf) {
   g_scan_trace = buf;
@@ -131,30 +126,15 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "reduce_waves")) {
     old = g_reduce_waves;
     g_reduce_waves = value;
-  } else if (!strcmp(name, "scan_l2")) {
-    old = g_scan_l2;
-    g_scan_l2 = value;
   } else if (!strcmp(name, "scan_l2dyn")) {
     old = g_scan_l2dyn;
     g_scan_l2dyn = value;
-  } else if (!strcmp(name, "scan_ahead")) {
-    old = g_scan_ahead;
-    g_scan_ahead = value;
-  } else if (!strcmp(name, "scan_ahead_subs")) {
-    old = g_scan_ahead_subs;
-    g_scan_ahead_subs = value;
   } else if (!strcmp(name, "scan_l2_subs")) {
     old = g_scan_l2_subs;
     g_scan_l2_subs = value;
   } else if (!strcmp(name, "scan_l2_min")) {
     old = g_scan_l2_min;
     g_scan_l2_min = value;
-  } else if (!strcmp(name, "scan_static")) {
-    old = g_scan_static;
-    g_scan_static = value;
-  } else if (!strcmp(name, "scan_ctas")) {
-    old = g_scan_ctas;
-    g_scan_ctas = value;
   } else if (!strcmp(name, "scan_sub")) {
     old = g_scan_sub;
     if (value >= 1 && value <= 4) g_scan_sub = value;
@@ -327,42 +307,13 @@ template <class T> struct TriadF {
   }
 };
 
-// Black-Scholes call (bench.py:102-116): vol = sigma*sqrt(T), disc = exp(-rT),
-// d1 = (log(S/K) + (r + sigma^2/2) T) / vol, d2 = d1 - vol,
-// price = S*Phi(d1) - K*disc*Phi(d2), Phi(x) = (1 + erf(x/sqrt 2))/2; vol <= 0 gives the
-// discounted intrinsic value max(S - K*disc, 0).  Computed in the element type.
-template <class T> struct BSMath;
-template <> struct BSMath<float> {
-  static __device__ __forceinline__ float price(float S, float K, float r, float v, float t) {
-    const float vol = v * sqrtf(t);
-    const float disc = expf(-r * t);
-    if (!(vol > 0.0f)) return fmaxf(S - K * disc, 0.0f);
-    const float d1 = (logf(S / K) + (r + 0.5f * v * v) * t) / vol;
-    const float d2 = d1 - vol;
-    const float n1 = 0.5f * (1.0f + erff(d1 * 0.70710678118654752f));
-    const float n2 = 0.5f * (1.0f + erff(d2 * 0.70710678118654752f));
-    return S * n1 - K * disc * n2;
-  }
-};
-template <> struct BSMath<double> {
-  static __device__ __forceinline__ double price(double S, double K, double r, double v, double t) {
-    const double vol = v * sqrt(t);
-    const double disc = exp(-r * t);
-    if (!(vol > 0.0)) return fmax(S - K * disc, 0.0);
-    const double d1 = (log(S / K) + (r + 0.5 * v * v) * t) / vol;
-    const double d2 = d1 - vol;
-    const double n1 = 0.5 * (1.0 + erf(d1 / 1.4142135623730951));
-    const double n2 = 0.5 * (1.0 + erf(d2 / 1.4142135623730951));
-    return S * n1 - K * disc * n2;
-  }
-};
-
 template <class T> struct BlackScholesF {
   struct Params {
     T* out;
     const T *S, *K, *r, *v, *t;
   };
   static constexpr int E = 16 / sizeof(T);
+  static constexpr int U = 1;  // transcendental-heavy: fewer registers, more warps
   struct Regs {
     T S[E], K[E], r[E], v[E], t[E];
   };
@@ -422,6 +373,9 @@ template <class T> struct GenF {
   static __device__ __forceinline__ void scalar(const Params& p, i64 i) { p.out[i] = gen(p, i); }
 };
 
+template <class F, class = void> struct UnrollOf { static constexpr int value = MAP_U; };
+template <class F> struct UnrollOf<F, decltype((void)F::U, void())> { static constexpr int value = F::U; };
+
 template <class F>
 static int launch_map(const typename F::Params& p, int64_t n, bool vec_ok, int device, void* stream,
                       const char* what) {
@@ -431,9 +385,10 @@ static int launch_map(const typename F::Params& p, int64_t n, bool vec_ok, int d
   cudaStream_t s = (cudaStream_t)stream;
   const int sms = sm_count(device);
   if (vec_ok) {
-    auto k = map_vec_kernel<F, BLOCK, MAP_U>;
+    constexpr int U = UnrollOf<F>::value;
+    auto k = map_vec_kernel<F, BLOCK, U>;
     const int64_t nchunk = n / F::E;
-    int64_t grid = (nchunk + (int64_t)BLOCK * MAP_U - 1) / ((int64_t)BLOCK * MAP_U);
+    int64_t grid = (nchunk + (int64_t)BLOCK * U - 1) / ((int64_t)BLOCK * U);
     if (g_map_waves > 0) {
       const int64_t cap = (int64_t)sms * occupancy(k, BLOCK, 0) * g_map_waves;
       if (grid > cap) grid = cap;
@@ -688,34 +643,10 @@ static uint64_t next_epoch(void* scratch) {
 }
 
 template <class T, class Op, int SUBS>
-static int launch_scan_ahead(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
-  constexpr int ITEMS = ScanItems<T, Op>::value;
-  constexpr int TILE = BLOCK * ITEMS * SUBS;
-  auto k = scan_ahead_kernel<T, Op, BLOCK, ITEMS, SUBS>;
-  const int smem = 2 * TILE * (int)sizeof(T);
-  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  int dev = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
-  if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
-  if (per_sm < 1) return -1;
-  const int64_t nt = (n + TILE - 1) / TILE;
-  auto p2 = p;
-  p2.ntiles = (u32)nt;
-  int64_t grid = (int64_t)sm_count(dev) * per_sm;
-  if (grid > nt) grid = nt;
-  void* args[] = {(void*)&p2};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
-  if (e == cudaSuccess) return 0;
-  cudaGetLastError();
-  return -1;
-}
-
-template <class T, class Op, int SUBS>
 static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int ITEMS = ScanItems<T, Op>::value;
   constexpr int TILE = BLOCK * ITEMS * SUBS;
-  auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, true>;
+  auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS>;
   const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
   DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int64_t nt = (n + TILE - 1) / TILE;
@@ -723,31 +654,6 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
   p2.ntiles = (u32)nt;
   k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
   return 0;
-}
-
-// Returns 0 on launch, an error code, or -1 when the cooperative launch is not possible.
-template <class T, class Op, int SUBS>
-static int launch_scan_l2(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
-  constexpr int ITEMS = ScanItems<T, Op>::value;
-  constexpr int TILE = BLOCK * ITEMS * SUBS;
-  auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS>;
-  const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
-  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  int dev = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
-  if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
-  if (per_sm < 1) return -1;
-  const int64_t nt = (n + TILE - 1) / TILE;
-  auto p2 = p;
-  p2.ntiles = (u32)nt;
-  int64_t grid = (int64_t)sm_count(dev) * per_sm;
-  if (grid > nt) grid = nt;
-  void* args[] = {(void*)&p2};
-  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
-  if (e == cudaSuccess) return 0;
-  cudaGetLastError();
-  return -1;
 }
 
 template <class T, class Op, int SUB>
@@ -765,44 +671,6 @@ static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& 
       case 12: return launch_scan_l2dyn<T, Op, 12>(p, n, s);
       case 16: return launch_scan_l2dyn<T, Op, 16>(p, n, s);
       default: return launch_scan_l2dyn<T, Op, 6>(p, n, s);
-    }
-  }
-  if (p.bulk_ok && g_scan_ahead && n >= (int64_t)g_scan_l2_min) {
-    int rc = -1;
-    switch (g_scan_ahead_subs) {
-      case 1: rc = launch_scan_ahead<T, Op, 1>(p, n, s); break;
-      case 3: rc = launch_scan_ahead<T, Op, 3>(p, n, s); break;
-      case 4: rc = launch_scan_ahead<T, Op, 4>(p, n, s); break;
-      default: rc = launch_scan_ahead<T, Op, 2>(p, n, s); break;
-    }
-    if (rc >= 0) return rc;
-  }
-  if (p.bulk_ok && g_scan_l2 && n >= (int64_t)g_scan_l2_min) {
-    int rc = -1;
-    switch (g_scan_l2_subs) {
-      case 2: rc = launch_scan_l2<T, Op, 2>(p, n, s); break;
-      case 4: rc = launch_scan_l2<T, Op, 4>(p, n, s); break;
-      case 8: rc = launch_scan_l2<T, Op, 8>(p, n, s); break;
-      default: rc = launch_scan_l2<T, Op, 6>(p, n, s); break;
-    }
-    if (rc >= 0) return rc;
-  }
-  if (p.bulk_ok && g_scan_static) {
-    constexpr int NS = 4, PF = 2;
-    auto k = scan_static_kernel<T, Op, BLOCK, ITEMS, SUB, NS, PF>;
-    const int smem = NS * C::IN_BYTES;
-    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int dev = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    DRK_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, BLOCK, smem));
-    if (g_scan_ctas > 0 && g_scan_ctas < per_sm) per_sm = g_scan_ctas;
-    int64_t grid = (int64_t)sm_count(dev) * per_sm;
-    if (grid > (int64_t)p.ntiles) grid = p.ntiles;
-    if (per_sm >= 1) {
-      void* args[] = {(void*)&p};
-      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3((unsigned)grid), dim3(BLOCK), args, smem, s);
-      if (e == cudaSuccess) return 0;
-      cudaGetLastError();  // fall through to the one-tile-per-CTA kernel
     }
   }
   auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS, SUB>;
@@ -904,4 +772,63 @@ extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* 
     return scan_op<T>(op, exclusive, (const T*)in, (T*)out, n, init_host, carry_host, carry_dev, seg_total_dev,
                       carry_out_dev, scratch, scratch_bytes, device, stream);
   });
+}
+
+// ---------------------------------------------------------------------------------------
+// scans of NVRTC-compiled kernels (custom associative operators)
+
+extern "C" int drk_jit_launch(void* handle, const char* kernel, unsigned grid, unsigned block, unsigned smem,
+                              const void* params, size_t params_bytes, int device, void* stream);
+
+template <class A>
+static int jit_scan_impl(void* handle, const char* kernel, int tile, int smem_bytes, int exclusive, const void* in,
+                         void* out, int64_t n, const void* init_host, const void* carry_host, const void* carry_dev,
+                         void* seg_total, void* carry_out, void* scratch, size_t scratch_bytes, int device,
+                         void* stream) {
+  if (n < 1 || tile < 1) return set_error(DRK_E_ARG, "drk_jit_scan: n and tile must be >= 1");
+  if (!in || !out) return set_error(DRK_E_ARG, "drk_jit_scan: null in/out");
+  if (exclusive && !init_host) return set_error(DRK_E_ARG, "drk_jit_scan: exclusive scan needs init");
+  if (carry_host && carry_dev) return set_error(DRK_E_ARG, "drk_jit_scan: give at most one carry");
+  const int64_t nt = (n + tile - 1) / tile;
+  if (!scratch || scratch_bytes < 128 + (size_t)nt * 16)
+    return set_error(DRK_E_SCRATCH, "drk_jit_scan: scratch too small");
+  ScanParams<A, const void*> p;
+  memset(&p, 0, sizeof(p));
+  p.in = in;
+  p.out = out;
+  p.n = n;
+  p.ntiles = (u32)nt;
+  p.exclusive = exclusive;
+  p.has_init = init_host != nullptr;
+  if (init_host) memcpy(&p.init, init_host, sizeof(A));
+  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
+  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
+  p.carry_ptr = (const A*)carry_dev;
+  p.seg_total = (A*)seg_total;
+  p.carry_out = (A*)carry_out;
+  p.counter = (u32*)scratch;
+  p.desc = (u64*)((char*)scratch + 128);
+  p.epoch = next_epoch(scratch);
+  p.bulk_ok = 0;
+  p.trace = nullptr;
+  return drk_jit_launch(handle, kernel, (unsigned)nt, BLOCK, (unsigned)smem_bytes, &p, sizeof(p), device, stream);
+}
+
+extern "C" size_t drk_jit_scan_scratch_bytes(int64_t n, int tile) {
+  if (n < 1) n = 1;
+  if (tile < 1) tile = 1;
+  return 128 + (size_t)((n + tile - 1) / tile) * 16;
+}
+
+extern "C" int drk_jit_scan(void* handle, const char* kernel, int acc_bytes, int tile, int smem_bytes, int exclusive,
+                            const void* in, void* out, int64_t n, const void* init_host, const void* carry_host,
+                            const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
+                            size_t scratch_bytes, int device, void* stream) {
+  if (acc_bytes == 8)
+    return jit_scan_impl<double>(handle, kernel, tile, smem_bytes, exclusive, in, out, n, init_host, carry_host,
+                                 carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes, device, stream);
+  if (acc_bytes == 4)
+    return jit_scan_impl<float>(handle, kernel, tile, smem_bytes, exclusive, in, out, n, init_host, carry_host,
+                                carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes, device, stream);
+  return set_error(DRK_E_ARG, "drk_jit_scan: acc_bytes must be 4 or 8");
 }

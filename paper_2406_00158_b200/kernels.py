@@ -63,6 +63,22 @@ def launch_kernel(name, launch_ctx, n, *args):
     _PROFILE.setdefault(name, []).append((s, e, n))
 
 
+def launch_jit(mod, kernel, grid, block, smem, buf, nbytes, lctx, n):
+    """Launch an NVRTC kernel (single packed-struct argument) on lctx's stream."""
+    args = (mod.handle, kernel.encode(), grid, block, smem, buf, nbytes, lctx.device, lctx.stream)
+    if _PROFILE is None:
+        _lib.call("drk_jit_launch", *args)
+        return
+    from .runtime import torch
+
+    t = torch()
+    s, e = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    s.record(lctx.state.stream)
+    _lib.call("drk_jit_launch", *args)
+    e.record(lctx.state.stream)
+    _PROFILE.setdefault("jit:" + kernel, []).append((s, e, n))
+
+
 class Launch:
     """Execution context of one segment: device, stream, device state, keep-alive list."""
 

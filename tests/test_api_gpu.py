@@ -1,0 +1,484 @@
+"""The segrange API on the device runtime (GPU).
+
+Same behaviours the reference's own tests pin (tests/test_algorithms.py, test_views.py,
+test_containers.py, test_bench.py of /root/reference/pkg), exercised through this
+package: element functions are traced to device kernels (AOT catalogue or NVRTC), so
+these tests also cover the code generator.  Expected values come from the reference's
+hand examples, from plain-Python folds, or from numpy on the same host data.
+"""
+
+import operator
+
+import numpy as np
+import pytest
+
+import paper_2406_00158_b200 as sr
+from paper_2406_00158_b200 import _lib, views
+from paper_2406_00158_b200.algorithms import BinaryOp, _scan_aligned, add, multiply
+from paper_2406_00158_b200 import bench as B
+from oracle import segrange_port as O
+
+pytestmark = pytest.mark.gpu
+
+
+def dvec(rt, values, partition=None, dtype=np.float64):
+    return sr.DistributedVector.from_numpy(rt, np.asarray(values, dtype=dtype), partition)
+
+
+def fold(values, op, init):
+    acc = init
+    for v in values:
+        acc = op(acc, v)
+    return acc
+
+
+# ---------------------------------------------------------------------------------------
+# for_each
+
+
+class TestForEach:
+    def test_increment(self, rt3):
+        v = dvec(rt3, [0, 1, 2])
+        sr.for_each(v, lambda x: x + 1)
+        assert v.to_numpy().tolist() == [1.0, 2.0, 3.0]
+
+    def test_stream_pattern_over_zip(self, rt3):
+        rng = np.random.default_rng(1)
+        a_data, b_data = rng.random(23), rng.random(23)
+        a, b = dvec(rt3, a_data), dvec(rt3, b_data)
+        sr.for_each(views.zip(a, b), lambda t: (t[0] + t[1], None))
+        assert a.to_numpy().tolist() == [x + y for x, y in zip(a_data.tolist(), b_data.tolist())]
+
+    def test_empty_range_launches_nothing(self, rt3):
+        k0 = _lib.launch_count()
+        sr.for_each(sr.DistributedVector(rt3, 0), lambda x: x)
+        assert _lib.launch_count() == k0
+
+    def test_vectorized_matches_elementwise(self, rt3):
+        data = np.linspace(-1, 1, 17)
+        a, b = dvec(rt3, data), dvec(rt3, data)
+        sr.for_each(a, lambda x: 3 * x + 1)
+        sr.for_each(b, lambda x: 3 * x + 1, vectorized=True)
+        assert np.array_equal(a.to_numpy(), b.to_numpy())
+        assert np.array_equal(a.to_numpy(), 3 * data + 1)
+
+    def test_vectorized_zip_writeback(self, rt3):
+        a = dvec(rt3, np.zeros(9))
+        b = dvec(rt3, np.arange(9))
+        sr.for_each(views.zip(a, b), lambda t: (t[1] * 2, None), vectorized=True)
+        assert a.to_numpy().tolist() == [2.0 * i for i in range(9)]
+
+    def test_read_only_target_rejected(self, rt3):
+        t = views.transform(dvec(rt3, [1, 2]), lambda x: x)
+        with pytest.raises(TypeError):
+            sr.for_each(t, lambda x: x + 1)
+
+    def test_side_effect_only_function_rejected(self, rt3):
+        seen = []
+        with pytest.raises(TypeError):
+            sr.for_each(dvec(rt3, [1, 2, 3]), lambda x: seen.append(x))
+
+    def test_branching_function_rejected(self, rt3):
+        with pytest.raises(TypeError):
+            sr.for_each(dvec(rt3, [1.0, -2.0]), lambda x: x if x > 0 else -x)
+
+    def test_plain_array_has_no_device(self):
+        with pytest.raises(TypeError):
+            sr.for_each(np.arange(5.0), lambda x: x + 1)
+
+    def test_write_into_list_fails_loudly(self, rt3):
+        v = sr.DistributedVector(rt3, 4)
+        with pytest.raises(TypeError):
+            sr.for_each(views.zip(v, [1.0, 2.0, 3.0, 4.0]), lambda t: (t[1], t[0]))
+
+    def test_read_from_host_list(self, rt3):
+        v = sr.DistributedVector(rt3, 4)
+        sr.for_each(views.zip(v, [1.0, 2.0, 3.0, 4.0]), lambda t: (t[1] * 2, None))
+        assert v.to_numpy().tolist() == [2.0, 4.0, 6.0, 8.0]
+
+    def test_two_outputs_one_kernel(self, rt3):
+        a = dvec(rt3, np.zeros(11))
+        b = dvec(rt3, np.zeros(11), dtype=np.int32)
+        c = dvec(rt3, np.arange(11))
+        sr.for_each(views.zip(a, b, c), lambda t: (t[2] * 0.5, t[2] * t[2], None), vectorized=True)
+        assert np.array_equal(a.to_numpy(), np.arange(11) * 0.5)
+        assert np.array_equal(b.to_numpy(), (np.arange(11) ** 2).astype(np.int32))
+
+    def test_shifted_self_read_is_snapshot(self, rt3):
+        # a[i] = a[i+1] through a zip of a with drop(a, 1): the reference materialises the
+        # right-hand side first (views.py:176), so the shift must not read updated values
+        data = np.arange(10.0)
+        a = dvec(rt3, data)
+        sr.for_each(views.zip(views.take(a, 9), views.drop(a, 1)), lambda t: (t[1], None), vectorized=True)
+        assert a.to_numpy().tolist() == list(data[1:]) + [9.0]
+
+
+# ---------------------------------------------------------------------------------------
+# reduce
+
+
+class TestReduce:
+    def test_sum_1_to_100(self, rt_pool):
+        for p in (1, 2, 3, 4, 7):
+            v = sr.DistributedVector.from_numpy(rt_pool(p), np.arange(1, 101, dtype=np.int64))
+            assert sr.reduce(v, 0) == 5050
+
+    def test_float_product_tolerance(self, rt_pool):
+        data = 1.0 + np.random.default_rng(5).random(200) / 100
+        r1 = sr.reduce(dvec(rt_pool(1), data), 1.0, multiply)
+        r4 = sr.reduce(dvec(rt_pool(4), data), 1.0, multiply)
+        assert abs(r4 - r1) / abs(r1) < 1e-12
+
+    def test_empty_returns_init(self, rt3):
+        assert sr.reduce(sr.DistributedVector(rt3, 0), 17) == 17
+
+    def test_matches_sequential_fold(self, rt_pool):
+        data = np.random.default_rng(9).random(1003)
+        expected = fold(data.tolist(), operator.add, 0.0)
+        for p in (1, 3, 7):
+            got = sr.reduce(dvec(rt_pool(p), data), 0.0)
+            assert abs(got - expected) / expected < 1e-12
+
+    def test_python_op_path(self, rt3):
+        v = dvec(rt3, [3, 1, 4, 1, 5], dtype=np.int64)
+        assert sr.reduce(v, 0, BinaryOp(lambda a, b: a + b)) == 14
+
+    def test_custom_callable_promoted(self, rt3):
+        v = dvec(rt3, [2, 3, 4], dtype=np.int64)
+        assert sr.reduce(v, 0, operator.add) == 9
+
+    def test_custom_associative_operator_jit(self, rt_pool):
+        data = np.random.default_rng(3).integers(-50, 50, 997).astype(np.int64)
+        op = lambda a, b: a + b + 1  # associative and commutative, not a ufunc
+        for p in (1, 4):
+            got = sr.reduce(dvec(rt_pool(p), data, dtype=np.int64), 0, op)
+            assert got == fold(data.tolist(), op, 0)
+
+    def test_min_max(self, rt3):
+        v = dvec(rt3, [5, -2, 9, 3], dtype=np.int64)
+        assert sr.reduce(v, 10**9, sr.minimum) == -2
+        assert sr.reduce(v, -(10**9), sr.maximum) == 9
+
+    def test_zip_elements_rejected(self, rt3):
+        with pytest.raises(TypeError):
+            sr.reduce(views.zip(dvec(rt3, [1, 2]), dvec(rt3, [3, 4])), 0)
+
+    def test_reduce_over_view_pipeline(self, rt3):
+        z = views.transform(views.zip(dvec(rt3, [1, 2, 3]), dvec(rt3, [4, 5, 6])), lambda t: t[0] * t[1])
+        assert sr.reduce(z, 0.0) == 32.0
+
+    def test_reduce_generic_expression_jit(self, rt3):
+        x = np.random.default_rng(2).random(5000)
+        v = dvec(rt3, x)
+        got = sr.reduce(views.transform(v, lambda e: np.sqrt(e) * 2.0 + np.exp(-e)), 0.0)
+        want = float(np.sum(np.sqrt(x) * 2.0 + np.exp(-x)))
+        assert abs(got - want) / want < 1e-12
+
+    def test_int32_sum_widens(self, rt3):
+        data = np.full(1000, 2**30, dtype=np.int32)
+        assert sr.reduce(dvec(rt3, data, dtype=np.int32), 0) == 1000 * 2**30
+
+
+# ---------------------------------------------------------------------------------------
+# scans
+
+
+class TestScans:
+    def test_hand_example_p2(self, rt_pool):
+        rt = rt_pool(2)
+        v = dvec(rt, [1, 2, 3, 4], dtype=np.int64)
+        out = sr.DistributedVector(rt, 4, init=0, dtype=np.int64)
+        partials = _scan_aligned(v, out, add, exclusive=False, init=None)
+        assert out.to_numpy().tolist() == [1, 3, 6, 10]
+        assert partials == [3, 7]
+
+    def test_single_element(self, rt3):
+        out = sr.DistributedVector(rt3, 1)
+        sr.inclusive_scan(dvec(rt3, [42]), out)
+        assert out.to_numpy().tolist() == [42.0]
+
+    def test_in_place_equals_out_of_place(self, rt3):
+        data = np.arange(11, dtype=np.int64)
+        a = dvec(rt3, data, dtype=np.int64)
+        out = sr.DistributedVector(rt3, 11, init=0, dtype=np.int64)
+        sr.inclusive_scan(a, out)
+        b = dvec(rt3, data, dtype=np.int64)
+        sr.inclusive_scan(b, b)
+        assert np.array_equal(out.to_numpy(), b.to_numpy())
+
+    def test_non_aligned_stages_through_temp(self, rt_pool):
+        rt = rt_pool(2)
+        v = dvec(rt, range(10), partition=[7, 3], dtype=np.int64)
+        out = sr.DistributedVector(rt, 10, init=0, dtype=np.int64, partition=[4, 6])
+        sr.inclusive_scan(v, out)
+        assert out.to_numpy().tolist() == np.cumsum(np.arange(10)).tolist()
+
+    def test_empty(self, rt3):
+        sr.inclusive_scan(sr.DistributedVector(rt3, 0), sr.DistributedVector(rt3, 0))
+
+    def test_length_mismatch(self, rt3):
+        with pytest.raises(ValueError):
+            sr.inclusive_scan(sr.DistributedVector(rt3, 3), sr.DistributedVector(rt3, 4))
+
+    def test_empty_segments(self, rt_pool):
+        rt = rt_pool(7)
+        out = sr.DistributedVector(rt, 4, init=0, dtype=np.int64)
+        sr.inclusive_scan(dvec(rt, [1, 2, 3, 4], dtype=np.int64), out)
+        assert out.to_numpy().tolist() == [1, 3, 6, 10]
+
+    def test_python_op(self, rt3):
+        out = sr.DistributedVector(rt3, 3, init=0, dtype=np.int64)
+        sr.inclusive_scan(dvec(rt3, [2, 3, 4], dtype=np.int64), out, BinaryOp(operator.mul, 1))
+        assert out.to_numpy().tolist() == [2, 6, 24]
+
+    def test_custom_operator_scan_jit(self, rt3):
+        data = np.random.default_rng(4).integers(-9, 9, 3001).astype(np.int64)
+        op = lambda a, b: a + b + 1
+        out = sr.DistributedVector(rt3, len(data), init=0, dtype=np.int64)
+        sr.inclusive_scan(dvec(rt3, data, dtype=np.int64), out, op)
+        acc, want = None, []
+        for x in data.tolist():
+            acc = x if acc is None else op(acc, x)
+            want.append(acc)
+        assert out.to_numpy().tolist() == want
+
+    def test_scan_from_view(self, rt3):
+        t = views.transform(dvec(rt3, [1, 2, 3, 4], dtype=np.int64), lambda x: x * 10)
+        out = sr.DistributedVector(rt3, 4, init=0, dtype=np.int64)
+        sr.inclusive_scan(t, out)
+        assert out.to_numpy().tolist() == [10, 30, 60, 100]
+
+    def test_exclusive_basic_and_init(self, rt_pool):
+        rt = rt_pool(3)
+        out = sr.DistributedVector(rt, 4, init=0, dtype=np.int64)
+        sr.exclusive_scan(dvec(rt, [1, 2, 3, 4], dtype=np.int64), out, 0)
+        assert out.to_numpy().tolist() == [0, 1, 3, 6]
+        for p in (1, 2, 5):
+            rt = rt_pool(p)
+            out = sr.DistributedVector(rt, 2, init=0, dtype=np.int64)
+            sr.exclusive_scan(dvec(rt, [1, 1], dtype=np.int64), out, 10)
+            assert out.to_numpy().tolist() == [10, 11]
+
+    def test_exclusive_plus_input_is_inclusive(self, rt_pool):
+        rng = np.random.default_rng(21)
+        for p in (1, 3, 7):
+            rt = rt_pool(p)
+            data = rng.integers(-20, 20, 31).astype(np.int64)
+            v = sr.DistributedVector.from_numpy(rt, data)
+            inc = sr.DistributedVector(rt, 31, init=0, dtype=np.int64)
+            exc = sr.DistributedVector(rt, 31, init=0, dtype=np.int64)
+            sr.inclusive_scan(v, inc)
+            sr.exclusive_scan(v, exc, 0)
+            assert (exc.to_numpy() + data).tolist() == inc.to_numpy().tolist()
+
+    @pytest.mark.parametrize("n", [1, 2, 255, 5119, 5120, 5121, 100_003, 1 << 22, (1 << 22) + 17])
+    def test_sizes_across_kernels_int32(self, rt_pool, n):
+        # crosses the single-pass (small) / L2 two-touch (>= 2^22) kernels and tile edges
+        x = O.mod_ints(7, 0, n, 2001, -1000).astype(np.int32)
+        for p in (1, 3):
+            rt = rt_pool(p)
+            out = sr.DistributedVector(rt, n, dtype=np.int32)
+            sr.inclusive_scan(dvec(rt, x, dtype=np.int32), out)
+            ref, _ = O.scan(x, p)
+            assert np.array_equal(out.to_numpy(), ref)
+            out2 = sr.DistributedVector(rt, n, dtype=np.int32)
+            sr.exclusive_scan(dvec(rt, x, dtype=np.int32), out2, 3)
+            ref2, _ = O.scan(x, p, exclusive=True, init=3)
+            assert np.array_equal(out2.to_numpy(), ref2)
+
+    def test_unaligned_slice_scan(self, rt3):
+        x = np.arange(1, 20001, dtype=np.int64)
+        v = dvec(rt3, x, dtype=np.int64)
+        d = views.drop(v, 3)
+        out = sr.DistributedVector(rt3, len(d), dtype=np.int64)
+        sr.inclusive_scan(d, out)
+        assert np.array_equal(out.to_numpy(), np.cumsum(x[3:]))
+
+    def test_min_max_scan(self, rt3):
+        x = np.random.default_rng(8).random(777)
+        out = sr.DistributedVector(rt3, 777)
+        sr.inclusive_scan(dvec(rt3, x), out, sr.maximum)
+        assert np.array_equal(out.to_numpy(), np.maximum.accumulate(x))
+
+
+# ---------------------------------------------------------------------------------------
+# copy / fill / transform / views
+
+
+class TestCopyAndViews:
+    def test_local_round_trip(self, rt3):
+        src = np.arange(10, dtype=np.float64)
+        v = sr.DistributedVector(rt3, 10)
+        back = np.zeros(10)
+        sr.copy(src, v)
+        sr.copy(v, back)
+        assert np.array_equal(src, back)
+
+    def test_repartition(self, rt_pool):
+        data = np.arange(23, dtype=np.float64)
+        v3 = sr.DistributedVector.from_numpy(rt_pool(3), data)
+        v4 = sr.DistributedVector(rt_pool(4), 23)
+        sr.copy(v3, v4)
+        assert np.array_equal(v4.to_numpy(), data)
+
+    def test_zero_length_and_mismatch(self, rt3):
+        sr.copy(sr.DistributedVector(rt3, 0), sr.DistributedVector(rt3, 0))
+        with pytest.raises(ValueError):
+            sr.copy(sr.DistributedVector(rt3, 3), sr.DistributedVector(rt3, 4))
+
+    def test_copy_from_view(self, rt3):
+        out = sr.DistributedVector(rt3, 8)
+        sr.copy(views.transform(dvec(rt3, range(8)), lambda x: x * x), out)
+        assert out.to_numpy().tolist() == [float(i * i) for i in range(8)]
+
+    def test_copy_from_zip_chunking(self, rt_pool):
+        rt = rt_pool(2)
+        a = dvec(rt, range(8), partition=[4, 4])
+        b = dvec(rt, range(8), partition=[3, 5])
+        out = sr.DistributedVector(rt, 8, partition=[2, 6])
+        sr.copy(views.transform(views.zip(a, b), lambda p: p[0] + p[1]), out)
+        assert out.to_numpy().tolist() == [2.0 * i for i in range(8)]
+
+    def test_copy_with_dtype_conversion(self, rt3):
+        src = dvec(rt3, [1.7, -2.2, 3.9])
+        out = sr.DistributedVector(rt3, 3, dtype=np.int32)
+        sr.copy(src, out)
+        assert out.to_numpy().tolist() == [1, -2, 3]
+
+    def test_fill_and_transform(self, rt3):
+        v = sr.DistributedVector(rt3, 7, dtype=np.float32)
+        sr.fill(v, 0.1)
+        assert np.array_equal(v.to_numpy(), np.full(7, 0.1, dtype=np.float32))
+        w = sr.DistributedVector(rt3, 7, dtype=np.float32)
+        sr.transform(v, w, lambda x: x * 3 + 1)
+        assert np.array_equal(w.to_numpy(), np.full(7, 0.1, dtype=np.float32) * 3 + 1)
+
+    def test_init_value(self, rt3):
+        v = sr.DistributedVector(rt3, 5, init=2.5)
+        assert v.to_numpy().tolist() == [2.5] * 5
+
+    def test_take_drop(self, rt3):
+        v = dvec(rt3, range(10))
+        assert sr.reduce(views.take(v, 4), 0.0) == 6.0
+        assert sr.reduce(views.drop(v, 7), 0.0) == 24.0
+
+    def test_enumerate_and_iota(self, rt3):
+        v = dvec(rt3, [10.0, 20.0, 30.0, 40.0])
+        e = views.enumerate(v)
+        assert sr.reduce(views.transform(e, lambda t: t[0] * t[1]), 0.0) == 200.0
+        w = sr.DistributedVector(rt3, 5, dtype=np.int64)
+        sr.copy(views.iota(3, 5), w)
+        assert w.to_numpy().tolist() == [3, 4, 5, 6, 7]
+
+    def test_relaxed_zip_write(self, rt_pool):
+        rt = rt_pool(2)
+        a = sr.DistributedVector(rt, 10, partition=[6, 4])
+        b = dvec(rt, range(10), partition=[3, 7])
+        sr.for_each(views.zip(a, b), lambda t: (t[1] + 1, None), vectorized=True)
+        assert a.to_numpy().tolist() == [float(i + 1) for i in range(10)]
+
+    def test_strict_zip_rejected(self, rt_pool):
+        rt = rt_pool(2)
+        a = sr.DistributedVector(rt, 10, partition=[6, 4])
+        b = sr.DistributedVector(rt, 10, partition=[3, 7])
+        with pytest.raises(sr.NonAlignedZip):
+            views.zip(a, b, mode="strict")
+
+    def test_element_access(self, rt3):
+        v = dvec(rt3, [1.5, 2.5, 3.5])
+        assert v[1] == 2.5
+        v[2] = 9.0
+        assert list(v) == [1.5, 2.5, 9.0]
+
+
+class TestJitExpressions:
+    """Generated kernels follow numpy's dtype rules and rounding."""
+
+    @pytest.mark.parametrize("fn", [
+        lambda x: x * 2.5 - 1.0,
+        lambda x: np.where(x > 0.5, x, -x),
+        lambda x: np.clip(x, 0.2, 0.7),
+        lambda x: np.floor(x * 10) / 10,
+        lambda x: (x * 7.0) % 3.0,
+        lambda x: (x * 7.0) // 3.0,
+        lambda x: x ** 2 + x ** 0.5,
+        lambda x: np.maximum(x, 0.3) + np.minimum(x, 0.6),
+        lambda x: np.abs(x - 0.5),
+    ])
+    def test_float_exact(self, rt3, fn):
+        x = np.random.default_rng(12).random(4099).astype(np.float32)
+        v = dvec(rt3, x, dtype=np.float32)
+        out = sr.DistributedVector(rt3, len(x), dtype=np.float32)
+        sr.transform(v, out, fn)
+        assert np.array_equal(out.to_numpy(), fn(x).astype(np.float32))
+
+    @pytest.mark.parametrize("fn", [
+        lambda x: np.sqrt(x) + np.exp(x) - np.log(x + 1.0),
+        lambda x: np.sin(x) * np.cos(x) + np.tanh(x),
+    ])
+    def test_float_transcendental(self, rt3, fn):
+        x = np.random.default_rng(13).random(4099)
+        out = sr.DistributedVector(rt3, len(x))
+        sr.transform(dvec(rt3, x), out, fn)
+        np.testing.assert_allclose(out.to_numpy(), fn(x), rtol=1e-13, atol=0)
+
+    @pytest.mark.parametrize("fn", [
+        lambda x: x * 3 - 7,
+        lambda x: x // 4,
+        lambda x: x % 5,
+        lambda x: -x,
+        lambda x: (x & 6) | 1,
+        lambda x: np.where(x > 0, x, 0),
+    ])
+    def test_int_exact(self, rt3, fn):
+        x = np.random.default_rng(14).integers(-1000, 1000, 4099).astype(np.int32)
+        out = sr.DistributedVector(rt3, len(x), dtype=np.int32)
+        sr.transform(dvec(rt3, x, dtype=np.int32), out, fn)
+        assert np.array_equal(out.to_numpy(), fn(x).astype(np.int32))
+
+    def test_int_true_divide_is_float64(self, rt3):
+        x = np.arange(1, 101, dtype=np.int32)
+        out = sr.DistributedVector(rt3, 100)
+        sr.transform(dvec(rt3, x, dtype=np.int32), out, lambda v: v / 3)
+        assert np.array_equal(out.to_numpy(), x / 3)
+
+    def test_black_scholes_as_traced_function(self, rt3):
+        n = 257
+        cols = [O.uniform_doubles(5, k * n, n, lo, hi) for k, (lo, hi) in enumerate(B.BS_RANGES.values())]
+        vecs = [dvec(rt3, c) for c in cols]
+        out = sr.DistributedVector(rt3, n)
+        B.black_scholes_prices(out, *vecs)
+        np.testing.assert_allclose(out.to_numpy(), O.black_scholes(*cols), rtol=1e-12)
+
+
+class TestRuntime:
+    def test_submit_and_wait_all(self, rt3):
+        tickets = [rt3.submit(k, lambda k=k: k * 10) for k in range(3)]
+        assert rt3.wait_all(tickets) == [0, 10, 20]
+
+    def test_aggregate_errors(self, rt3):
+        def bad():
+            raise ValueError("boom")
+
+        tickets = [rt3.submit(0, lambda: 1), rt3.submit(1, bad), rt3.submit(2, bad)]
+        with pytest.raises(sr.AggregateTaskError) as ei:
+            rt3.wait_all(tickets)
+        assert [i for i, _ in ei.value.failures] == [1, 2]
+
+    def test_copy_between_handles(self, rt3):
+        a = rt3.allocate(0, 5, np.float32)
+        b = rt3.allocate(2, 5, np.float32)
+        rt3.copy(np.arange(5, dtype=np.float32), a)
+        rt3.copy(a, b)
+        host = np.zeros(5, dtype=np.float32)
+        rt3.copy(b, host)
+        assert host.tolist() == [0.0, 1.0, 2.0, 3.0, 4.0]
+        with pytest.raises(ValueError):
+            rt3.copy(a, rt3.allocate(1, 4, np.float32))
+
+    def test_local_view_guard(self, rt3):
+        v = dvec(rt3, [1.0, 2.0, 3.0])
+        seg = v.segments()[1]
+        with pytest.raises(sr.OffLocaleAccess):
+            sr.local_view(seg)
+        assert rt3.wait_all([rt3.submit(seg.rank, lambda: sr.local_view(seg).shape[0])]) == [1]
