@@ -116,7 +116,7 @@ def for_each(r, fn, vectorized: bool = False) -> None:
         value = lw.value if vectorized else _promote_python(lw.value)
         key = _views._value_key(value)
         if key not in cache:
-            cache[key] = expr.trace(fn, value)
+            cache[key] = expr.trace_cached(fn, value, key)
         result = cache[key]
         if result is None:
             raise TypeError(

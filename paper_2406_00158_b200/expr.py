@@ -100,8 +100,17 @@ class Node:
         return f"{self.op}({', '.join(map(repr, self.args))}):{self.dtype}"
 
 
+_LEAVES = {}
+
+
 def leaf(slot: int, dtype) -> Node:
-    return Node("leaf", (), dtype, slot)
+    """Interned leaf node (so structural keys of repeated lowerings are cached)."""
+    dt = np.dtype(dtype)
+    key = (slot, dt.str)
+    n = _LEAVES.get(key)
+    if n is None:
+        n = _LEAVES[key] = Node("leaf", (), dt, slot)
+    return n
 
 
 def index_node() -> Node:
@@ -186,10 +195,25 @@ def _operand(x):
 
 def _weak_type(v):
     if isinstance(v, bool):
-        return bool
+        return np.dtype(np.bool_)  # Python bools are not weak under NEP 50
     if isinstance(v, int):
         return int
     return float
+
+
+_LOOPS = {}
+
+
+def _resolve(uf, name, descr):
+    key = (name, tuple(d.str if isinstance(d, np.dtype) else d.__name__ for d in descr))
+    loop = _LOOPS.get(key)
+    if loop is None:
+        try:
+            loop = uf.resolve_dtypes(tuple(descr) + (None,))
+        except Exception as exc:
+            raise TraceError(f"numpy has no {name} loop for {descr}: {exc}") from None
+        _LOOPS[key] = loop
+    return loop
 
 
 def apply_ufunc(name: str, *xs):
@@ -213,10 +237,7 @@ def apply_ufunc(name: str, *xs):
             return xs[0]
         if p == -1:
             return apply_ufunc("reciprocal", xs[0])
-    try:
-        loop = uf.resolve_dtypes(tuple(descr) + (None,))
-    except Exception as exc:
-        raise TraceError(f"numpy has no {name} loop for {descr}: {exc}") from None
+    loop = _resolve(uf, name, descr)
     args = []
     for (node, scalar), dt in zip(nodes, loop[:-1]):
         if node is None:
@@ -452,6 +473,43 @@ def to_nodes(result):
     if isinstance(result, np.ndarray) and result.ndim == 0:
         return const(result.item(), result.dtype)
     raise TraceError(f"element function returned {type(result).__name__}; expected element values")
+
+
+_TRACES = {}
+_TRACE_CACHE_MAX = 4096
+
+
+def _fn_key(fn):
+    """A hashable identity of a function's behaviour: code, defaults, closure contents and
+    the referenced globals.  None if any of those is unhashable (no caching then)."""
+    code = getattr(fn, "__code__", None)
+    if code is None:
+        return None
+    try:
+        cells = tuple(c.cell_contents for c in (fn.__closure__ or ()))
+        g = fn.__globals__
+        glob = tuple((nm, g[nm]) for nm in code.co_names if nm in g and not callable(g[nm])
+                     and not hasattr(g[nm], "__dict__"))
+        key = (code, fn.__defaults__, cells, glob)
+        hash(key)
+        return key
+    except Exception:
+        return None
+
+
+def trace_cached(fn, value, value_key):
+    """trace() memoised on (function identity, lowered value structure)."""
+    fk = _fn_key(fn)
+    if fk is None:
+        return trace(fn, value)
+    key = (fk, value_key)
+    out = _TRACES.get(key)
+    if out is None:
+        out = trace(fn, value)
+        if len(_TRACES) >= _TRACE_CACHE_MAX:
+            _TRACES.clear()
+        _TRACES[key] = out
+    return out
 
 
 def trace(fn, value):

@@ -1,0 +1,135 @@
+"""Tracer dtype rules against numpy itself, traceability errors, AOT catalogue matching,
+and NVRTC compilation of generated kernels (compile only: no GPU needed)."""
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_2406_00158_b200 as sr
+from paper_2406_00158_b200 import codegen, expr, kernels, views
+from paper_2406_00158_b200 import bench as B
+
+DTYPES = [np.float32, np.float64, np.int32, np.int64]
+OPS = [
+    lambda a, b: a + b, lambda a, b: a - b, lambda a, b: a * b, lambda a, b: a / b,
+    lambda a, b: np.maximum(a, b), lambda a, b: a > b, lambda a, b: np.where(a > b, a, b),
+]
+SCALARS = [2, 3.5, True, np.float32(1.5), np.int64(3)]
+
+
+def sym(dt, slot=0):
+    return expr.Sym(expr.leaf(slot, dt))
+
+
+@given(st.sampled_from(DTYPES), st.sampled_from(DTYPES), st.integers(0, len(OPS) - 1))
+@settings(max_examples=120)
+def test_binary_dtype_matches_numpy(da, db, k):
+    op = OPS[k]
+    a, b = np.ones(3, dtype=da), np.ones(3, dtype=db)
+    want = np.asarray(op(a, b)).dtype
+    got = op(sym(da), sym(db, 1))
+    assert got.dtype == want
+
+
+@given(st.sampled_from(DTYPES), st.sampled_from(SCALARS), st.integers(0, 5))
+@settings(max_examples=120)
+def test_weak_scalar_dtype_matches_numpy(da, s, k):
+    op = OPS[k]
+    a = np.ones(3, dtype=da)
+    with np.errstate(all="ignore"):
+        want = np.asarray(op(a, s)).dtype
+        got = op(sym(da), s)
+    assert got.dtype == want
+
+
+@pytest.mark.parametrize("fn,dt", [
+    (np.sqrt, np.float32), (np.sqrt, np.int32), (np.exp, np.float64), (np.floor_divide, np.int64),
+    (np.abs, np.int32), (np.square, np.float32), (np.negative, np.int64),
+])
+def test_ufunc_dtype(fn, dt):
+    a = np.ones(3, dtype=dt)
+    x = sym(dt)
+    if fn is np.floor_divide:
+        assert fn(x, 3).dtype == fn(a, 3).dtype
+    else:
+        assert fn(x).dtype == fn(a).dtype
+
+
+def test_triad_traces_to_two_roundings():
+    node = expr.trace(lambda t: (t[1] + 3.0 * t[2], None, None),
+                      (expr.leaf(0, np.float32), expr.leaf(1, np.float32), expr.leaf(2, np.float32)))
+    assert node[0].op == "add" and node[0].dtype == np.float32
+    assert node[0].args[1].op == "multiply" and node[0].args[1].args[0].value == 3.0
+
+
+@pytest.mark.parametrize("fn", [
+    lambda x: x if x > 0 else -x,
+    lambda x: float(x),
+    lambda x: np.asarray(x),
+    lambda x: [v for v in x],
+    lambda x: x[0],
+])
+def test_untraceable_functions_raise(fn):
+    with pytest.raises(expr.TraceError):
+        expr.trace(fn, expr.leaf(0, np.float64))
+
+
+def test_trace_cache_respects_closures():
+    out = []
+    for alpha in (2.0, 3.0):
+        f = lambda x, a=alpha: x * a  # noqa: E731
+        g = (lambda a: (lambda x: x * a))(alpha)
+        n1 = expr.trace_cached(f, expr.leaf(0, np.float64), ("k",))
+        n2 = expr.trace_cached(g, expr.leaf(0, np.float64), ("k",))
+        out.append((n1.args[1].value, n2.args[1].value))
+    assert out == [(2.0, 2.0), (3.0, 3.0)]
+
+
+def _lowered(meta_rt, dtypes, n=16):
+    vecs = [sr.DistributedVector(meta_rt[1], n, dtype=d) for d in dtypes]
+    z = views.zip(*vecs)
+    return views.lower(z.segments()[0])
+
+
+@pytest.mark.parametrize("fn,kernel", [
+    (lambda t: (t[1] + 3.0 * t[2], None, None), "drk_triad"),
+    (lambda t: (3.0 * t[2] + t[1], None, None), "drk_triad"),
+    (lambda t: (t[1] * 2.0, None, None), "drk_scale"),
+    (lambda t: (t[1] + t[2], None, None), "drk_add"),
+    (lambda t: (t[1], None, None), "drk_copy"),
+    (lambda t: (0.5, None, None), "drk_fill"),
+    (lambda t: (np.sqrt(t[1]), None, None), None),
+])
+def test_catalogue_matching(meta_rt, fn, kernel):
+    lw = _lowered(meta_rt, [np.float32] * 3)
+    res = expr.trace(fn, lw.value)
+    m = kernels.match_map(res[0], lw.leaves, np.float32)
+    assert (m[0] if m else None) == kernel
+
+
+def test_black_scholes_catalogue(meta_rt):
+    lw = _lowered(meta_rt, [np.float32] * 6)
+    res = expr.trace(lambda t: (B.black_scholes_call(t[1], t[2], t[3], t[4], t[5]),) + (None,) * 5, lw.value)
+    assert kernels.match_map(res[0], lw.leaves, np.float32)[0] == "drk_black_scholes"
+
+
+def test_codegen_compiles_map_reduce_scan(meta_rt):
+    lw = _lowered(meta_rt, [np.float32, np.float64, np.int32])
+    res = expr.trace(lambda t: (np.where(t[0] > 0.5, np.sqrt(t[1]), t[2] // 3), t[2] % 7 + 1, None), lw.value)
+    writes = [(lw.target[0], res[0]), (lw.target[1], res[1])]
+    src = codegen._map_source(writes, lw.leaves)[0]
+    assert len(codegen.cubin_for(src, "map.cu")) > 1000
+    op = sr.BinaryOp(lambda a, b: a + b + 1)
+    opname, opsrc = codegen._op_struct(None, op, np.dtype(np.int64))
+    assert "OpC" in opsrc
+    mod_src = f'#include "drk_device.cuh"\n{opsrc}\nextern "C" __global__ void k(const drk::ScanParams<long long, ' \
+              f'const long long*> p) {{ drk::scan_kernel_body<drk::PlainLoad<long long>, long long, OpC, 256, 10, 1>(p); }}'
+    assert len(codegen.cubin_for(mod_src, "scan.cu")) > 1000
+
+
+def test_match_binary():
+    assert codegen.match_binary(lambda a, b: a + b, np.dtype(np.int64)) == 0
+    assert codegen.match_binary(lambda a, b: b * a, np.dtype(np.float64)) == 1
+    assert codegen.match_binary(lambda a, b: np.minimum(a, b), np.dtype(np.float64)) == 2
+    assert codegen.match_binary(lambda a, b: a + b + 1, np.dtype(np.int64)) is None
