@@ -110,6 +110,8 @@ static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
 static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned segments
 static int g_scan_l2_min = 1 << 22;
 static int g_scan_l2_subs = 6;   // sub-tiles per L2 tile (120 KB for fp32)
+static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
+                                 // measured slower than one 120 KB tile per CTA
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
 extern "C" int drk_scan_set_trace(void* buf) {
   g_scan_trace = buf;
@@ -132,6 +134,9 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2_subs")) {
     old = g_scan_l2_subs;
     g_scan_l2_subs = value;
+  } else if (!strcmp(name, "scan_l2_pipe")) {
+    old = g_scan_l2_pipe;
+    g_scan_l2_pipe = value;
   } else if (!strcmp(name, "scan_l2_min")) {
     old = g_scan_l2_min;
     g_scan_l2_min = value;
@@ -642,18 +647,40 @@ static uint64_t next_epoch(void* scratch) {
   return ++g_scan_epochs[(uintptr_t)scratch];
 }
 
-template <class T, class Op, int SUBS>
+template <class T, class Op, int SUBS, int ITEMS>
 static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
-  constexpr int ITEMS = ScanItems<T, Op>::value;
   constexpr int TILE = BLOCK * ITEMS * SUBS;
-  auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS>;
   const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
-  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int64_t nt = (n + TILE - 1) / TILE;
   auto p2 = p;
   p2.ntiles = (u32)nt;
-  k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
+  if (g_scan_l2_pipe) {
+    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, true>;
+    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int64_t grid = (int64_t)sm_count(dev) * occupancy(k, BLOCK, smem);
+    if (grid > nt) grid = nt;
+    k<<<(unsigned)grid, BLOCK, smem, s>>>(p2);
+  } else {
+    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, false>;
+    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
+  }
   return 0;
+}
+
+// Large aligned segments: L2 two-touch scan.  The variant (sub-tile items, sub-tiles per
+// tile) is a tuning knob; defaults measured best on B200.
+template <class T, class Op>
+static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+  constexpr int IT = ScanItems<T, Op>::value;
+  switch (g_scan_l2_subs) {
+    case 2: return launch_scan_l2dyn<T, Op, 2, IT>(p, n, s);
+    case 3: return launch_scan_l2dyn<T, Op, 3, IT>(p, n, s);
+    case 4: return launch_scan_l2dyn<T, Op, 4, IT>(p, n, s);
+    default: return launch_scan_l2dyn<T, Op, 6, IT>(p, n, s);
+  }
 }
 
 template <class T, class Op, int SUB>
@@ -663,16 +690,7 @@ static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& 
   const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
   if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
   p.ntiles = (u32)nt64;
-  if (p.bulk_ok && g_scan_l2dyn && n >= (int64_t)g_scan_l2_min) {
-    switch (g_scan_l2_subs) {
-      case 2: return launch_scan_l2dyn<T, Op, 2>(p, n, s);
-      case 4: return launch_scan_l2dyn<T, Op, 4>(p, n, s);
-      case 8: return launch_scan_l2dyn<T, Op, 8>(p, n, s);
-      case 12: return launch_scan_l2dyn<T, Op, 12>(p, n, s);
-      case 16: return launch_scan_l2dyn<T, Op, 16>(p, n, s);
-      default: return launch_scan_l2dyn<T, Op, 6>(p, n, s);
-    }
-  }
+  if (p.bulk_ok && g_scan_l2dyn && n >= (int64_t)g_scan_l2_min) return launch_scan_l2_any<T, Op>(p, n, s);
   auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS, SUB>;
   if (C::SMEM > 48 * 1024) DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   k<<<p.ntiles, BLOCK, C::SMEM, s>>>(p);
