@@ -407,9 +407,28 @@ def _grid(mod, kernel, work, device):
     return int(max(1, min(cap, work)))
 
 
+_MAP_PLANS = {}
+_REDUCE_PLANS = {}
+_PLAN_MAX = 2048
+
+
+def _leaf_sig(leaves, used):
+    return tuple((k, leaves[k].kind, leaves[k].dtype.str) for k in sorted(used))
+
+
 def run_map(writes, leaves, ptrs, n, launch):
-    src, words, out_w, leaf_w, E, U, array_slots = _map_source(writes, leaves)
-    mod = compile_module(src, "drk_map.cu")
+    key = (tuple((np.dtype(t.dtype).str, node.key()) for t, node in writes),
+           _leaf_sig(leaves, expr.leaves_used(tuple(n_ for _, n_ in writes))))
+    plan = _MAP_PLANS.get(key)
+    if plan is None:
+        src, words, out_w, leaf_w, E, U, array_slots = _map_source(writes, leaves)
+        plan = (compile_module(src, "drk_map.cu"), list(words.values), out_w, leaf_w, E, U, array_slots)
+        if len(_MAP_PLANS) >= _PLAN_MAX:
+            _MAP_PLANS.clear()
+        _MAP_PLANS[key] = plan
+    mod, wvals, out_w, leaf_w, E, U, array_slots = plan
+    words = Words()
+    words.values = list(wvals)
     for j, (tgt, _) in enumerate(writes):
         words.values[out_w[j]] = tgt.ptr()
     for k, w in leaf_w.items():
@@ -473,6 +492,38 @@ def match_binary(fn, dtype):
 
 def run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot):
     V = np.dtype(node.dtype)
+    fk = expr._fn_key(combiner.fn) if (opcode is None and combiner is not None) else None
+    cacheable = opcode is not None or fk is not None
+    key = (node.key(), _leaf_sig(leaves, expr.leaves_used(node)), opcode, fk)
+    plan = _REDUCE_PLANS.get(key) if cacheable else None
+    if plan is None:
+        plan = _reduce_plan(node, leaves, opcode, combiner, V)
+        if cacheable:
+            if len(_REDUCE_PLANS) >= _PLAN_MAX:
+                _REDUCE_PLANS.clear()
+            _REDUCE_PLANS[key] = plan
+    mod, wvals, leaf_w, E, array_slots, opcode = plan
+    words = Words()
+    words.values = list(wvals)
+    for k, w in leaf_w.items():
+        words.values[w] = ptrs[k] if leaves[k].kind != "index" else leaves[k].base
+    vec_ok = all(ptrs[k] % 16 == 0 for k in array_slots)
+    st = launch.state
+    scratch = st.reduce_scratch.data_ptr()
+    res = st.result_dev_ptr(slot)
+    blob = (words.pack() + struct.pack("<qi4x", n, 1 if vec_ok else 0)
+            + struct.pack("<QQQ", scratch, scratch + 128, scratch + 128 + 4096 * 8)
+            + struct.pack("<QQ", res, 0))
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    work = (n // E if vec_ok else n) // (BLOCK * 4) + 1
+    grid = min(_grid(mod, "drk_reduce", work, launch.device) // 8, 4096)
+    from .kernels import launch_jit
+
+    launch_jit(mod, "drk_reduce", max(1, grid), BLOCK, 0, buf, len(blob), launch, n)
+    return opcode
+
+
+def _reduce_plan(node, leaves, opcode, combiner, V):
     if opcode is None and combiner is not None:
         code = match_binary(combiner.fn, V)
         if code is not None:
@@ -502,8 +553,12 @@ def run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot):
     T = ctype(V)
     regs = "\n".join(f"    {ctype(leaves[k].dtype)} a{k}[E];\n    drk::ldv<{ctype(leaves[k].dtype)}, E>("
                      f"(const {ctype(leaves[k].dtype)}*)p.w[{leaf_w[k]}] + i, a{k});" for k in array_slots)
-    nwords = max(1, len(words.values))
+    if not words.values:
+        words.add(0)
+    nwords = len(words.values)
     A = _acc_ctype(V, opcode)
+    nl = "\n      "
+    nl4 = "\n    "
     src = f'''#include "drk_device.cuh"
 {opsrc}
 struct LD {{
@@ -516,12 +571,12 @@ struct LD {{
     for (int e = 0; e < E; ++e) {{
       const long long gi = i + e;
       (void)gi;
-      {(chr(10) + "      ").join(ev.lines)}
+      {nl.join(ev.lines)}
       v[e] = (V)({rv});
     }}
   }}
   static __device__ __forceinline__ V one(const Params& p, long long i) {{
-    {(chr(10) + "    ").join(es.lines)}
+    {nl4.join(es.lines)}
     return (V)({rs});
   }}
 }};
@@ -531,24 +586,7 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) drk_reduce(const RArgs a) 
 }}
 '''
     mod = compile_module(src, "drk_reduce.cu")
-    for k, w in leaf_w.items():
-        words.values[w] = ptrs[k] if leaves[k].kind != "index" else leaves[k].base
-    if not words.values:
-        words.add(0)
-    vec_ok = all(ptrs[k] % 16 == 0 for k in array_slots)
-    st = launch.state
-    scratch = st.reduce_scratch.data_ptr()
-    res = st.result_dev_ptr(slot)
-    blob = (words.pack() + struct.pack("<qi4x", n, 1 if vec_ok else 0)
-            + struct.pack("<QQQ", scratch, scratch + 128, scratch + 128 + 4096 * 8)
-            + struct.pack("<QQ", res, 0))
-    buf = ctypes.create_string_buffer(blob, len(blob))
-    work = (n // E if vec_ok else n) // (BLOCK * 4) + 1
-    grid = min(_grid(mod, "drk_reduce", work, launch.device) // 8 * 1, 4096)
-    from .kernels import launch_jit
-
-    launch_jit(mod, "drk_reduce", max(1, grid), BLOCK, 0, buf, len(blob), launch, n)
-    return opcode
+    return (mod, list(words.values), leaf_w, E, array_slots, opcode)
 
 
 def _acc_ctype(V, opcode):
