@@ -45,7 +45,7 @@ STEP_WORKLOADS = ("dot", "triad", "scan")
 def parse():
     p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--log2n", type=int, default=30, help="elements per GPU = 2^log2n (default 30)")
@@ -141,15 +141,23 @@ class ClockSampler:
 
 
 def dist_setup(gpus):
+    """One process per GPU (torchrun).  DRK_BENCH_SHARE_GPU=1 is a test mode for hosts with
+    one GPU: every rank uses GPU 0 and the exchange runs over gloo (NCCL refuses two ranks
+    on one device); timings from that mode are not measurements."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("DRK_BENCH_SHARE_GPU") == "1":
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("DRK_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -166,7 +174,8 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
