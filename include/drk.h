@@ -113,6 +113,18 @@ int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_
              void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
              int device, void* stream);
 
+/* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
+ * Device radix sort (CUB) of one contiguous buffer; the runtime gathers a distributed
+ * vector's segments into it and writes the sorted run back in segment order.
+ * With scratch == NULL, *scratch_bytes receives the required scratch size. */
+int drk_sort_keys(int dtype, void* keys, void* alt, int64_t n, void* scratch, size_t* scratch_bytes,
+                  int device, void* stream);
+/* stable sort of (key, int64 index) pairs by key; idx receives the sorting permutation */
+int drk_sort_pairs(int key_dtype, void* keys, void* keys_alt, void* idx, void* idx_alt, int64_t n,
+                   void* scratch, size_t* scratch_bytes, int device, void* stream);
+/* out[i] = in[idx[i]] (idx: int64) */
+int drk_gather(int dtype, void* out, const void* in, const void* idx, int64_t n, int device, void* stream);
+
 /* ---- tuning / introspection ------------------------------------------------------------ */
 /* set a launch parameter by name ("map_waves", "reduce_waves"); returns the old value */
 int drk_tune(const char* name, int value);

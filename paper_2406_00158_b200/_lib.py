@@ -76,6 +76,9 @@ SIGNATURES = {
     "drk_dot": (_int, [_int, _vp, _vp, _i64, _vp, _vp, _int, _vp]),
     "drk_scan_scratch_bytes": (_sz, [_int, _int, _i64]),
     "drk_scan": (_int, [_int, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
+    "drk_sort_keys": (_int, [_int, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
+    "drk_sort_pairs": (_int, [_int, _vp, _vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
+    "drk_gather": (_int, [_int, _vp, _vp, _vp, _i64, _int, _vp]),
     "drk_tune": (_int, [_cp, _int]),
     "drk_scan_set_trace": (_int, [_vp]),
     "drk_launch_count": (_i64, []),

@@ -16,6 +16,7 @@ host.
 
 from __future__ import annotations
 
+import ctypes
 import operator
 from dataclasses import dataclass
 
@@ -389,6 +390,106 @@ def _check_carry_range(op, partials, live, exclusive, init, T, carry=None):
             failures.append((j, OverflowError(f"Python integer {int(seed)} out of bounds for {T}")))
     if failures:
         raise AggregateTaskError(failures)
+
+
+# ----------------------------------------------------------------------------------------
+# sort
+
+
+def sort(r, key=None) -> None:
+    """In-place ascending sort of a distributed vector (algorithms.py:315-432); with `key`,
+    a stable sort by key(x) (the key function is traced like any element function).
+
+    The segments are gathered into one buffer on the first segment's GPU (peer copies over
+    NVLink for segments on other GPUs), radix-sorted there (CUB, library code: sort is not
+    on the benchmarked path) and written back in segment order.  A multi-GPU sample sort
+    with an all-to-all exchange is the scalable version of this."""
+    from .containers import VectorSegment
+    from .runtime import torch, torch_dtype
+
+    segs = segments_of(r)
+    for s_ in segs:
+        if not isinstance(s_, VectorSegment):
+            raise TypeError("sort needs raw writable storage segments")
+    live = [s_ for s_ in segs if len(s_)]
+    total = sum(len(s_) for s_ in live)
+    if total <= 1:
+        return
+    rt = _require_runtime(runtime_of(r), "sort")
+    T = np.dtype(live[0].dtype)
+    code = _lib.dtype_code(T)
+    states = {rt.state_of(s_.rank).index: rt.state_of(s_.rank) for s_ in live}
+    for st in states.values():
+        st.synchronize()  # pending writes of every segment land before the gather
+    st0 = rt.state_of(live[0].rank)
+    t = torch()
+    with t.cuda.stream(st0.stream):
+        buf = t.empty(total, dtype=torch_dtype(T), device=st0.device)
+        alt = t.empty(total, dtype=torch_dtype(T), device=st0.device)
+    off = 0
+    for s_ in live:
+        _lib.call("drk_memcpy_async", buf.data_ptr() + off * T.itemsize, s_.data_ptr(), len(s_) * T.itemsize,
+                  st0.index, st0.handle)
+        off += len(s_)
+    launch = Launch(st0)
+    need = ctypes.c_size_t(0)
+    if key is None:
+        _lib.call("drk_sort_keys", code, buf.data_ptr(), alt.data_ptr(), total, None, ctypes.byref(need),
+                  st0.index, st0.handle)
+        with t.cuda.stream(st0.stream):
+            scratch = t.empty(max(1, need.value), dtype=t.uint8, device=st0.device)
+        _lib.call("drk_sort_keys", code, buf.data_ptr(), alt.data_ptr(), total, scratch.data_ptr(),
+                  ctypes.byref(need), st0.index, st0.handle)
+        result = buf
+    else:
+        node = expr.trace_cached(key, expr.leaf(0, T), ("sortkey", T.str))
+        if node is None or isinstance(node, tuple):
+            raise TypeError("sort key must return one value per element")
+        K = np.dtype(node.dtype)
+        if K not in _lib.DTYPE_CODE:
+            node, K = expr.cast(node, np.int32 if K.kind == "b" else np.float64), np.dtype(
+                np.int32 if K.kind == "b" else np.float64)
+        with t.cuda.stream(st0.stream):
+            kbuf = t.empty(total, dtype=torch_dtype(K), device=st0.device)
+            kalt = t.empty(total, dtype=torch_dtype(K), device=st0.device)
+            idx = t.empty(total, dtype=t.int64, device=st0.device)
+            idx_alt = t.empty(total, dtype=t.int64, device=st0.device)
+        tgt = _DeviceTarget(kbuf, K, st0.index)
+        run_map([(tgt, node)], [kernels._TensorLeaf(buf, T, total)], total, launch)
+        _lib.call("drk_iota", _lib.I64, idx.data_ptr(), total, 0, st0.index, st0.handle)
+        _lib.call("drk_sort_pairs", _lib.DTYPE_CODE[K], kbuf.data_ptr(), kalt.data_ptr(), idx.data_ptr(),
+                  idx_alt.data_ptr(), total, None, ctypes.byref(need), st0.index, st0.handle)
+        with t.cuda.stream(st0.stream):
+            scratch = t.empty(max(1, need.value), dtype=t.uint8, device=st0.device)
+        _lib.call("drk_sort_pairs", _lib.DTYPE_CODE[K], kbuf.data_ptr(), kalt.data_ptr(), idx.data_ptr(),
+                  idx_alt.data_ptr(), total, scratch.data_ptr(), ctypes.byref(need), st0.index, st0.handle)
+        _lib.call("drk_gather", code, alt.data_ptr(), buf.data_ptr(), idx.data_ptr(), total, st0.index, st0.handle)
+        result = alt
+    off = 0
+    for s_ in live:
+        _lib.call("drk_memcpy_async", s_.data_ptr(), result.data_ptr() + off * T.itemsize, len(s_) * T.itemsize,
+                  st0.index, st0.handle)
+        off += len(s_)
+    st0.synchronize()
+
+
+class _DeviceTarget(Target):
+    """A write target over a raw device tensor (temporaries of sort)."""
+
+    def __init__(self, tensor, dtype, device):
+        self.handle = None
+        self.start = 0
+        self.length = tensor.numel()
+        self.dtype = np.dtype(dtype)
+        self._t = tensor
+        self._device = device
+
+    def ptr(self):
+        return self._t.data_ptr()
+
+    @property
+    def device(self):
+        return self._device
 
 
 # ----------------------------------------------------------------------------------------

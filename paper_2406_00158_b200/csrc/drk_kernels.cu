@@ -41,6 +41,8 @@ static int cuda_status(cudaError_t e, const char* what) {
   } while (0)
 
 extern "C" const char* drk_last_error(void) { return g_last_error.c_str(); }
+int drk_error(int code, const char* msg) { return set_error(code, msg); }
+int drk_cuda_error(cudaError_t e, const char* what) { return cuda_status(e, what); }
 extern "C" int drk_version(void) { return 1; }
 extern "C" int64_t drk_launch_count(void) { return g_launches.load(); }
 extern "C" int64_t drk_note_launch(void) { return g_launches.fetch_add(1) + 1; }
@@ -850,3 +852,4 @@ extern "C" int drk_jit_scan(void* handle, const char* kernel, int acc_bytes, int
                                 carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes, device, stream);
   return set_error(DRK_E_ARG, "drk_jit_scan: acc_bytes must be 4 or 8");
 }
+

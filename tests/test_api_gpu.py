@@ -482,3 +482,53 @@ class TestRuntime:
         with pytest.raises(sr.OffLocaleAccess):
             sr.local_view(seg)
         assert rt3.wait_all([rt3.submit(seg.rank, lambda: sr.local_view(seg).shape[0])]) == [1]
+
+
+class TestSort:
+    """reference tests/test_algorithms.py TestSort cases"""
+
+    def test_reverse_sorted(self, rt3):
+        v = dvec(rt3, list(reversed(range(10))))
+        sr.sort(v)
+        assert v.to_numpy().tolist() == [float(i) for i in range(10)]
+
+    def test_random_u64_like_keys(self, rt4):
+        keys = O.splitmix64(99, 0, 100_000).astype(np.int64)
+        v = sr.DistributedVector.from_numpy(rt4, keys)
+        sr.sort(v)
+        assert v.to_numpy().tolist() == sorted(keys.tolist())
+
+    def test_all_equal_and_two_valued(self, rt_pool):
+        for p in (1, 4, 7):
+            v = sr.DistributedVector.from_numpy(rt_pool(p), np.full(500, 3.0))
+            sr.sort(v)
+            assert (v.to_numpy() == 3.0).all()
+        data = np.random.default_rng(2).choice([1.0, 2.0], size=1000)
+        v = sr.DistributedVector.from_numpy(rt_pool(4), data)
+        sr.sort(v)
+        out = v.to_numpy()
+        assert (np.diff(out) >= 0).all() and (out == 1.0).sum() == (data == 1.0).sum()
+
+    def test_key_function_stable(self, rt3):
+        v = dvec(rt3, [-5, 3, -1, 4, -2, 1, -3])
+        sr.sort(v, key=lambda x: np.abs(x))
+        assert v.to_numpy().tolist() == [-1.0, 1.0, -2.0, 3.0, -3.0, 4.0, -5.0]
+
+    def test_short_and_zero_length_segments(self, rt_pool):
+        v = dvec(rt_pool(7), [3, 1, 2])
+        sr.sort(v)
+        assert v.to_numpy().tolist() == [1.0, 2.0, 3.0]
+        data = np.random.default_rng(6).integers(0, 99, 8).astype(np.int64)
+        w = sr.DistributedVector.from_numpy(rt_pool(4), data, partition=[0, 5, 0, 3])
+        sr.sort(w)
+        assert w.to_numpy().tolist() == sorted(data.tolist())
+
+    def test_sort_view_rejected(self, rt3):
+        with pytest.raises(TypeError):
+            sr.sort(views.transform(dvec(rt3, [2, 1]), lambda x: x))
+
+    def test_float32_large(self, rt3):
+        x = O.unit_doubles(4, 0, 1 << 20).astype(np.float32)
+        v = dvec(rt3, x, dtype=np.float32)
+        sr.sort(v)
+        assert np.array_equal(v.to_numpy(), np.sort(x))
