@@ -287,6 +287,10 @@ template <class T> struct AddF {
   }
 };
 
+#ifndef BS_E
+#define BS_E 2  // 16-byte vectors per operand per thread (ILP of the transcendental chain)
+#endif
+
 // a = b + alpha * c with numpy's two roundings (weak-scalar alpha already in T).
 template <class T> struct TriadF {
   struct Params {
@@ -319,7 +323,7 @@ template <class T> struct BlackScholesF {
     T* out;
     const T *S, *K, *r, *v, *t;
   };
-  static constexpr int E = 16 / sizeof(T);
+  static constexpr int E = BS_E * 16 / sizeof(T);
   static constexpr int U = 1;  // transcendental-heavy: fewer registers, more warps
   struct Regs {
     T S[E], K[E], r[E], v[E], t[E];
