@@ -26,7 +26,7 @@ from . import _lib, expr, kernels
 from . import views as _views
 from .containers import DistributedVector
 from .core import has_segments, is_aligned, runtime_of, segments_of
-from .kernels import OPCODES, Launch, run_map, run_reduce, run_scan, stage_leaves
+from .kernels import OPCODES, Launch, run_map, run_reduce, run_scan
 from .runtime import AggregateTaskError
 from .views import ReadOnly, Target, ZipView, lower
 
@@ -550,21 +550,9 @@ def _copy_to_host(rt, ls, piece, launches):
     t = torch()
     with t.cuda.stream(st.stream):
         tmp = t.empty(ls.length, dtype=torch_dtype(host.dtype), device=st.device)
-    h = _views.Target.__new__(_views.Target)
-    h.handle, h.start, h.length, h.dtype = _TmpHandle(tmp, st.index), 0, ls.length, np.dtype(host.dtype)
-    run_map([(h, node)], ls.leaves, ls.length, launch)
+    run_map([(_DeviceTarget(tmp, host.dtype, st.index), node)], ls.leaves, ls.length, launch)
     st.synchronize()
     host[...] = tmp.cpu().numpy()
-
-
-class _TmpHandle:
-    def __init__(self, tensor, device):
-        self._t = tensor
-        self.device_index = device
-        self.locale = None
-
-    def data_ptr(self):
-        return self._t.data_ptr()
 
 
 def fill(r, value) -> None:

@@ -42,10 +42,6 @@ class JitError(TypeError):
     """An expression could not be compiled to a device kernel."""
 
 
-class JitUnavailable(JitError):
-    pass
-
-
 def ctype(dt) -> str:
     dt = np.dtype(dt)
     key = dt.kind + str(dt.itemsize)

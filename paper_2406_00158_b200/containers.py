@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _lib
 from .core import Distribution
-from .runtime import torch, torch_dtype, _np_dtype_of
+from .runtime import torch, torch_dtype
 from .views import Leaf, Lowered, Target
 from . import expr
 

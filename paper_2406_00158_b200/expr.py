@@ -17,9 +17,6 @@ None), or materialise their input (``np.asarray(x)``) cannot be traced; they rai
 
 from __future__ import annotations
 
-import math
-import operator
-
 import numpy as np
 
 try:  # scipy.special.erf is a ufunc; the reference's norm_cdf uses it (bench.py:19,102-103)
@@ -111,10 +108,6 @@ def leaf(slot: int, dtype) -> Node:
     if n is None:
         n = _LEAVES[key] = Node("leaf", (), dt, slot)
     return n
-
-
-def index_node() -> Node:
-    return Node("index", (), np.int64, 0)
 
 
 def const(value, dtype) -> Node:

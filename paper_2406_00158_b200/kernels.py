@@ -15,8 +15,8 @@ import ctypes
 
 import numpy as np
 
-from . import _lib, expr
-from .views import Leaf, Target
+from . import _lib
+from .views import Leaf
 
 OPCODES = {"add": _lib.ADD, "multiply": _lib.MUL, "minimum": _lib.MIN, "maximum": _lib.MAX}
 

@@ -240,7 +240,6 @@ class TaskTicket:
     def done(self) -> bool:
         if self._done:
             return True
-        t = torch()
         return all(st.stream is None or st.stream.query() for st in self._states)
 
     def exception(self, timeout=None):
