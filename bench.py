@@ -426,7 +426,11 @@ def main():
 
 
 def run_e2e(args, rt, st, world, rank, group, workloads, dt):
-    """The step through the public API with host inputs/outputs in pinned memory."""
+    """The step through the public API from pinned host memory: uploads of b and c, the
+    three pipelines, downloads of the triad and scan outputs (and the dot scalar), every
+    step.  Transfers use the asynchronous API (upload/to_numpy with wait=False) on
+    double-buffered device vectors, so step i+1's host->device copies overlap step i's
+    device->host copies — the two PCIe directions — and the kernels wait on the device."""
     import torch
 
     import paper_2406_00158_b200 as sr
@@ -437,60 +441,61 @@ def run_e2e(args, rt, st, world, rank, group, workloads, dt):
         import psutil
 
         avail = psutil.virtual_memory().available
-        while (3 << log2n) * 4 * world > 0.4 * avail and log2n > 20:
+        while (4 << log2n) * 4 * world > 0.4 * avail and log2n > 20:
             log2n -= 1
     except Exception:
         pass
     n = 1 << log2n
-    from oracle import segrange_port as _unused  # noqa: F401  (host data below is plain numpy)
-
-    hb = sr.pinned_empty(n, dt)
-    hc = sr.pinned_empty(n, dt)
-    ha = sr.pinned_empty(n, dt)
+    hb, hc = sr.pinned_empty(n, dt), sr.pinned_empty(n, dt)
+    ha, ho = sr.pinned_empty(n, dt), sr.pinned_empty(n, dt)
     rng = np.random.default_rng(rank)
     hb[...] = rng.random(n, dtype=np.float32)
     hc[...] = rng.random(n, dtype=np.float32)
-    a = sr.DistributedVector(rt, n, dtype=dt)
-    b = sr.DistributedVector(rt, n, dtype=dt)
-    c = sr.DistributedVector(rt, n, dtype=dt)
+    sets = [tuple(sr.DistributedVector(rt, n, dtype=dt) for _ in range(4)) for _ in range(2)]
     sw = [w for w in workloads if w in ("dot", "triad", "scan")]
-    h2d = d2h = 0
+    tickets = []
+    h2d = 2 * n * 4
+    d2h = (8 if "dot" in sw else 0) + n * 4 * (("triad" in sw) + ("scan" in sw))
 
-    def step():
-        nonlocal h2d, d2h
-        b.upload(hb)
-        c.upload(hc)
-        h2d = 2 * n * 4
-        d2h = 0
+    def step(i):
+        a, b, c, o = sets[i % 2]
+        tickets.append(b.upload(hb, wait=False))
+        tickets.append(c.upload(hc, wait=False))
         if "dot" in sw:
             z = views.transform(views.zip(b, c), lambda t: t[0] * t[1])
             spmd.reduce(z, 0.0, A.add, group) if group else A.reduce(z, 0.0, A.add)
-            d2h += 8
         if "triad" in sw:
             B.stream_triad(a, b, c)
-            a.to_numpy(out=ha)
-            d2h += n * 4
+            tickets.append(a.to_numpy(out=ha, wait=False)[1])
         if "scan" in sw:
-            spmd.inclusive_scan(c, a, group) if group else A.inclusive_scan(c, a)
-            a.to_numpy(out=ha)
-            d2h += n * 4
+            spmd.inclusive_scan(c, o, group) if group else A.inclusive_scan(c, o)
+            tickets.append(o.to_numpy(out=ho, wait=False)[1])
 
-    step()
+    def drain():
+        for tk in tickets:
+            tk.wait()
+        tickets.clear()
+
+    step(0)
+    step(1)
+    drain()
     torch.cuda.synchronize()
     barrier(world)
     steps = max(3, min(args.steps, 10))
     t0 = time.perf_counter()
-    for _ in range(steps):
-        step()
+    for i in range(steps):
+        step(i)
+    drain()
     torch.cuda.synchronize()
     dtm = (time.perf_counter() - t0) / steps
     dtm = max_over_ranks(dtm, world)
     nbytes = sum(BYTES[w] for w in sw) * n * world
-    del a, b, c
+    del sets
     return {"value": round(nbytes / dtm / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "elements_per_gpu": n, "ms_per_step": round(dtm * 1e3, 3),
-            "note": "same step via the public API; H2D of inputs from pinned host memory and D2H of outputs "
-                    "inside the timed region (wall clock, max over ranks)"}
+            "note": "same step via the public API from pinned host memory; every step uploads b and c and "
+                    "downloads both outputs (+ the dot scalar) inside the timed region; async transfers on "
+                    "double-buffered vectors overlap the two PCIe directions (wall clock, max over ranks)"}
 
 
 if __name__ == "__main__":

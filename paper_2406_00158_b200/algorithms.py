@@ -294,6 +294,9 @@ def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
             raise TypeError("scan needs scalar elements; apply a transform to the zip first")
         plain = node.op == "leaf" and lw.leaves[node.value].kind == "array" and node.dtype == tgt.dtype
         if plain and lw.leaves[node.value].device == st.index:
+            from .runtime import await_pending
+
+            await_pending(st, [lw.leaves[node.value].handle, tgt.handle])
             in_ptr = lw.leaves[node.value].ptr()
         else:
             run_map([(tgt, node)], lw.leaves, lw.length, launch)
@@ -419,6 +422,10 @@ def sort(r, key=None) -> None:
     T = np.dtype(live[0].dtype)
     code = _lib.dtype_code(T)
     states = {rt.state_of(s_.rank).index: rt.state_of(s_.rank) for s_ in live}
+    from .runtime import await_pending
+
+    for s_ in live:
+        await_pending(rt.state_of(s_.rank), [s_.handle])
     for st in states.values():
         st.synchronize()  # pending writes of every segment land before the gather
     st0 = rt.state_of(live[0].rank)

@@ -105,9 +105,12 @@ class VectorSegment:
     def to_numpy(self) -> np.ndarray:
         out = np.empty(self.length, dtype=self.handle.dtype)
         if self.length:
+            from .runtime import await_pending
+
             rt = self.handle.runtime
             rt._check_compute()
             st = rt.state_of(self.handle.locale)
+            await_pending(st, [self.handle])
             _lib.call("drk_memcpy_async", out.ctypes.data, self.data_ptr(), out.nbytes, st.index, st.handle)
             st.synchronize()
         return out
@@ -194,8 +197,16 @@ class DistributedVector:
         self._starts = np.array([d.global_offset for d in distribution.descriptors], dtype=np.int64)
 
     # -- host <-> device -----------------------------------------------------------------
-    def upload(self, array: np.ndarray, wait: bool = True) -> None:
-        """Copy a host array of length n into the segments (H2D on every segment stream)."""
+    def upload(self, array: np.ndarray, wait: bool = True):
+        """Copy a host array of length n into the segments.
+
+        wait=True: synchronous (returns None).  wait=False: asynchronous on each GPU's
+        host->device copy stream, returning a TransferTicket; the array must stay alive and
+        unchanged until then.  Kernels that later touch the vector wait for the copy on
+        the device (no host sync), and the copy itself waits for work already enqueued on
+        the vector, so transfers overlap compute and the opposite PCIe direction."""
+        from .runtime import TransferTicket, await_pending
+
         array = np.asarray(array)
         if array.shape != (self.n,):
             raise ValueError(f"upload expects shape ({self.n},), got {array.shape}")
@@ -206,8 +217,7 @@ class DistributedVector:
             raise RuntimeError("backend='meta' vectors hold no data")
         array = np.ascontiguousarray(array)
         pinned = array.nbytes >= _PIN_THRESHOLD and is_pinned(array)
-        staged = []
-        used = set()
+        staged, events, used = [], [], {}
         for h, d in zip(self.storage, self.distribution.descriptors):
             if not d.length:
                 continue
@@ -218,25 +228,46 @@ class DistributedVector:
                 buf[...] = src
                 staged.append(buf)
                 src = buf
-            _lib.call("drk_memcpy_async", h.data_ptr(), src.ctypes.data, src.nbytes, st.index, st.handle)
-            used.add(st.index)
-        if wait or staged:
-            for dev in used:
-                rt.device_state(dev).synchronize()
+            if wait:
+                await_pending(st, [h])
+                _lib.call("drk_memcpy_async", h.data_ptr(), src.ctypes.data, src.nbytes, st.index, st.handle)
+                used[st.index] = st
+            else:
+                cs = st.copy_stream("h2d")
+                cs.wait_event(st.compute_event())  # earlier kernels on this vector finish first
+                for ev in h._pending:
+                    cs.wait_event(ev)
+                _lib.call("drk_memcpy_async", h.data_ptr(), src.ctypes.data, src.nbytes, st.index,
+                          int(cs.cuda_stream))
+                ev = torch().cuda.Event()
+                ev.record(cs)
+                h._pending = [ev]
+                events.append(ev)
+        if wait:
+            for st in used.values():
+                st.synchronize()
+            return None
+        return TransferTicket(events, keep=(array, staged))
 
-    def to_numpy(self, out: np.ndarray | None = None) -> np.ndarray:
-        """Gather all segments into a host array (D2H on every segment stream)."""
+    def to_numpy(self, out: np.ndarray | None = None, wait: bool = True):
+        """Gather all segments into a host array.
+
+        wait=True returns the array.  wait=False enqueues the device->host copies on each
+        GPU's d2h copy stream after the work already enqueued on the vector and returns
+        (array, TransferTicket); the array is valid after ticket.wait().  Kernels that later
+        overwrite the vector wait for the copy on the device."""
+        from .runtime import TransferTicket, await_pending
+
         rt = self.runtime
         if out is None:
             out = np.empty(self.n, dtype=self.dtype)
         elif out.shape != (self.n,) or out.dtype != self.dtype:
             raise ValueError("to_numpy: out has the wrong shape or dtype")
         if self.n == 0:
-            return out
+            return out if wait else (out, TransferTicket([]))
         rt._check_compute()
         direct = out.nbytes >= _PIN_THRESHOLD and is_pinned(out)
-        pending = []
-        used = set()
+        pending, events, used = [], [], {}
         for h, d in zip(self.storage, self.distribution.descriptors):
             if not d.length:
                 continue
@@ -246,13 +277,32 @@ class DistributedVector:
                 buf = pinned_empty(d.length, self.dtype)
                 pending.append((dst, buf))
                 dst = buf
-            _lib.call("drk_memcpy_async", dst.ctypes.data, h.data_ptr(), dst.nbytes, st.index, st.handle)
-            used.add(st.index)
-        for dev in used:
-            rt.device_state(dev).synchronize()
-        for dst, buf in pending:
-            dst[...] = buf
-        return out
+            if wait:
+                await_pending(st, [h])
+                _lib.call("drk_memcpy_async", dst.ctypes.data, h.data_ptr(), dst.nbytes, st.index, st.handle)
+                used[st.index] = st
+            else:
+                cs = st.copy_stream("d2h")
+                cs.wait_event(st.compute_event())
+                for ev in h._pending:
+                    cs.wait_event(ev)
+                _lib.call("drk_memcpy_async", dst.ctypes.data, h.data_ptr(), dst.nbytes, st.index,
+                          int(cs.cuda_stream))
+                ev = torch().cuda.Event()
+                ev.record(cs)
+                h._pending = [ev]
+                events.append(ev)
+
+        def finish():
+            for dst, buf in pending:
+                dst[...] = buf
+
+        if wait:
+            for st in used.values():
+                st.synchronize()
+            finish()
+            return out
+        return out, TransferTicket(events, keep=(out,), finish=finish)
 
     # -- segments / indexing -----------------------------------------------------------------
     def segments(self) -> list:

@@ -95,6 +95,9 @@ def stage_leaves(leaves, launch: Launch):
     """Make every leaf readable by a kernel on launch.device: host slices are copied to
     the device (asynchronously, on the segment stream).  Returns per-leaf pointers (0 for
     index leaves)."""
+    from .runtime import await_pending
+
+    await_pending(launch.state, [lf.handle for lf in leaves if lf.kind == "array" and lf.handle is not None])
     ptrs = []
     for lf in leaves:
         if lf.kind == "array":
@@ -186,6 +189,9 @@ def run_map(writes, leaves, n, launch: Launch):
     """Write each (Target, node) of `writes` for n elements on launch's device."""
     if n == 0 or not writes:
         return
+    from .runtime import await_pending
+
+    await_pending(launch.state, [t.handle for t, _ in writes if t.handle is not None])
     leaves = _dealias(writes, leaves, n, launch)
     ptrs = stage_leaves(leaves, launch)
     if len(writes) == 1:

@@ -152,6 +152,60 @@ class DeviceState:
         if self.backend == "cuda":
             _lib.call("drk_stream_synchronize", self.index, self.handle)
 
+    # -- asynchronous host transfers ---------------------------------------------
+    def copy_stream(self, direction: str):
+        """Dedicated stream for host->device ("h2d") or device->host ("d2h") copies, so
+        transfers in both PCIe directions overlap each other and the compute stream."""
+        name = "_" + direction + "_stream"
+        s = getattr(self, name, None)
+        if s is None:
+            s = torch().cuda.Stream(device=self.device)
+            setattr(self, name, s)
+        return s
+
+    def compute_event(self):
+        """An event recorded now on the compute stream."""
+        ev = torch().cuda.Event()
+        ev.record(self.stream)
+        return ev
+
+
+def await_pending(state, handles):
+    """Make the compute stream of `state` wait for in-flight asynchronous transfers of any
+    of `handles` (uploads writing them, downloads still reading them)."""
+    for h in handles:
+        pend = getattr(h, "_pending", None)
+        if pend:
+            for ev in pend:
+                state.stream.wait_event(ev)
+            pend.clear()
+
+
+class TransferTicket:
+    """Completion of an asynchronous upload / download; wait() blocks until it is done
+    (and runs the host-side finisher of staged copies, if any)."""
+
+    __slots__ = ("_events", "_keep", "_finish", "_done")
+
+    def __init__(self, events, keep=(), finish=None):
+        self._events = list(events)
+        self._keep = keep
+        self._finish = finish
+        self._done = False
+
+    def wait(self):
+        if not self._done:
+            for ev in self._events:
+                ev.synchronize()
+            if self._finish is not None:
+                self._finish()
+            self._done = True
+            self._keep = ()
+        return None
+
+    def done(self) -> bool:
+        return self._done or all(ev.query() for ev in self._events)
+
 
 class StorageHandle:
     """Zero-initialised device storage owned by one locale (reference runtime.py:61-105).
@@ -159,7 +213,7 @@ class StorageHandle:
     ``span()`` returns the 1-D device tensor; ``read``/``write`` move single elements
     between host and device (convenience only, synchronous)."""
 
-    __slots__ = ("locale", "length", "dtype", "runtime", "_tensor", "_freed", "__weakref__")
+    __slots__ = ("locale", "length", "dtype", "runtime", "_tensor", "_freed", "_pending", "__weakref__")
 
     def __init__(self, runtime, locale: LocaleId, length: int, dtype, tensor):
         self.runtime = runtime
@@ -168,6 +222,7 @@ class StorageHandle:
         self.dtype = np.dtype(dtype)
         self._tensor = tensor
         self._freed = False
+        self._pending = []  # events of in-flight async transfers touching this storage
 
     def span(self):
         if self._freed:
@@ -184,13 +239,16 @@ class StorageHandle:
     def read(self, i: int):
         t = self.span()
         self.runtime._check_compute()
-        self.runtime.state_of(self.locale).synchronize()
+        st = self.runtime.state_of(self.locale)
+        await_pending(st, [self])
+        st.synchronize()
         return t[i].item()
 
     def write(self, i: int, value):
         t = self.span()
         self.runtime._check_compute()
         st = self.runtime.state_of(self.locale)
+        await_pending(st, [self])
         buf = np.asarray([value]).astype(self.dtype)
         host = torch().from_numpy(buf)
         with torch().cuda.stream(st.stream):

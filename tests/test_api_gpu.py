@@ -532,3 +532,43 @@ class TestSort:
         v = dvec(rt3, x, dtype=np.float32)
         sr.sort(v)
         assert np.array_equal(v.to_numpy(), np.sort(x))
+
+
+class TestAsyncTransfers:
+    def test_async_upload_then_compute(self, rt3):
+        n = 1 << 20
+        host = sr.pinned_empty(n, np.float32)
+        host[...] = np.arange(n, dtype=np.float32) % 7
+        v = sr.DistributedVector(rt3, n, dtype=np.float32)
+        tk = v.upload(host, wait=False)
+        total = sr.reduce(v, 0.0)  # waits for the copy on the device
+        tk.wait()
+        assert total == float(np.sum(host, dtype=np.float64))
+
+    def test_async_download_not_clobbered(self, rt3):
+        n = 1 << 20
+        v = dvec(rt3, np.arange(n, dtype=np.float32) % 5, dtype=np.float32)
+        out = sr.pinned_empty(n, np.float32)
+        res, tk = v.to_numpy(out=out, wait=False)
+        sr.fill(v, 9.0)  # must wait for the download on the device
+        tk.wait()
+        assert np.array_equal(res, np.arange(n, dtype=np.float32) % 5)
+        assert (v.to_numpy() == 9.0).all()
+
+    def test_pipelined_steps(self, rt3):
+        n = 1 << 18
+        hb = sr.pinned_empty(n, np.float32)
+        hb[...] = 1.0
+        outs, tks = [], []
+        vecs = [sr.DistributedVector(rt3, n, dtype=np.float32) for _ in range(2)]
+        for i in range(6):
+            v = vecs[i % 2]
+            tks.append(v.upload(hb, wait=False))
+            sr.inclusive_scan(v, v)
+            o = np.empty(n, dtype=np.float32)
+            outs.append(o)
+            tks.append(v.to_numpy(out=o, wait=False)[1])
+        for tk in tks:
+            tk.wait()
+        for o in outs:
+            assert np.array_equal(o, np.arange(1, n + 1, dtype=np.float32))
