@@ -111,7 +111,8 @@ static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
 static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
 static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned segments
 static int g_scan_l2_min = 1 << 22;
-static int g_scan_l2_subs = 6;   // sub-tiles per L2 tile (120 KB for fp32)
+static int g_scan_l2_subs = 8;   // sub-tiles per L2 tile (160 KB for fp32)
+static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
 static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
                                  // measured slower than one 120 KB tile per CTA
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
@@ -136,6 +137,9 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2_subs")) {
     old = g_scan_l2_subs;
     g_scan_l2_subs = value;
+  } else if (!strcmp(name, "scan_l2_ring")) {
+    old = g_scan_l2_ring;
+    g_scan_l2_ring = value;
   } else if (!strcmp(name, "scan_l2_pipe")) {
     old = g_scan_l2_pipe;
     g_scan_l2_pipe = value;
@@ -653,15 +657,15 @@ static uint64_t next_epoch(void* scratch) {
   return ++g_scan_epochs[(uintptr_t)scratch];
 }
 
-template <class T, class Op, int SUBS, int ITEMS>
+template <class T, class Op, int SUBS, int ITEMS, int RING>
 static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int TILE = BLOCK * ITEMS * SUBS;
-  const int smem = 3 * BLOCK * ITEMS * (int)sizeof(T);
+  const int smem = RING * BLOCK * ITEMS * (int)sizeof(T);
   const int64_t nt = (n + TILE - 1) / TILE;
   auto p2 = p;
   p2.ntiles = (u32)nt;
   if (g_scan_l2_pipe) {
-    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, true>;
+    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, true, RING>;
     DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int dev = 0;
     cudaGetDevice(&dev);
@@ -669,23 +673,21 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
     if (grid > nt) grid = nt;
     k<<<(unsigned)grid, BLOCK, smem, s>>>(p2);
   } else {
-    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, false>;
+    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, false, RING>;
     DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
   }
   return 0;
 }
 
-// Large aligned segments: L2 two-touch scan.  The variant (sub-tile items, sub-tiles per
-// tile) is a tuning knob; defaults measured best on B200.
 template <class T, class Op>
 static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int IT = ScanItems<T, Op>::value;
   switch (g_scan_l2_subs) {
-    case 2: return launch_scan_l2dyn<T, Op, 2, IT>(p, n, s);
-    case 3: return launch_scan_l2dyn<T, Op, 3, IT>(p, n, s);
-    case 4: return launch_scan_l2dyn<T, Op, 4, IT>(p, n, s);
-    default: return launch_scan_l2dyn<T, Op, 6, IT>(p, n, s);
+    case 6: return launch_scan_l2dyn<T, Op, 6, IT, 3>(p, n, s);
+    case 10: return launch_scan_l2dyn<T, Op, 10, IT, 3>(p, n, s);
+    case 12: return launch_scan_l2dyn<T, Op, 12, IT, 3>(p, n, s);
+    default: return launch_scan_l2dyn<T, Op, 8, IT, 3>(p, n, s);
   }
 }
 
