@@ -25,6 +25,9 @@ extern "C" {
 
 /* element types (numpy dtypes float32, float64, int32, int64) */
 enum { DRK_F32 = 0, DRK_F64 = 1, DRK_I32 = 2, DRK_I64 = 3 };
+/* unsigned element types: sort / gather / bounds only (the reference's sort bench sorts
+ * uint64 splitmix64 keys, bench.py:332-345) */
+enum { DRK_U32 = 4, DRK_U64 = 5 };
 /* binary operators (reference algorithms.py:47-50: add, multiply, minimum, maximum) */
 enum { DRK_ADD = 0, DRK_MUL = 1, DRK_MIN = 2, DRK_MAX = 3 };
 /* generator kinds for drk_generate (reference repro.py:21-40) */
@@ -114,16 +117,22 @@ int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_
              int device, void* stream);
 
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
- * Device radix sort (CUB) of one contiguous buffer; the runtime gathers a distributed
- * vector's segments into it and writes the sorted run back in segment order.
+ * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),
+ * plus the splitter search of the distributed sample sort; the runtime moves the runs
+ * between GPUs (peer copies) exactly as the reference's redistribution does.
  * With scratch == NULL, *scratch_bytes receives the required scratch size. */
 int drk_sort_keys(int dtype, void* keys, void* alt, int64_t n, void* scratch, size_t* scratch_bytes,
                   int device, void* stream);
-/* stable sort of (key, int64 index) pairs by key; idx receives the sorting permutation */
+/* stable sort of (key, int64 index) pairs by key, in place: keys end sorted, idx permuted alongside */
 int drk_sort_pairs(int key_dtype, void* keys, void* keys_alt, void* idx, void* idx_alt, int64_t n,
                    void* scratch, size_t* scratch_bytes, int device, void* stream);
 /* out[i] = in[idx[i]] (idx: int64) */
 int drk_gather(int dtype, void* out, const void* in, const void* idx, int64_t n, int device, void* stream);
+/* sample-sort redistribution bounds (algorithms.py:371-378 `_count_task` on a sorted run):
+ * bounds[j] = searchsorted(sorted[0:n], split[j], side="right") in numpy's order (NaN last);
+ * split (dtype) and bounds (int64) are device arrays of nsplit entries */
+int drk_sort_bounds(int dtype, const void* sorted, int64_t n, const void* split, int nsplit, void* bounds,
+                    int device, void* stream);
 
 /* ---- tuning / introspection ------------------------------------------------------------ */
 /* set a launch parameter by name ("map_waves", "reduce_waves"); returns the old value */

@@ -18,6 +18,7 @@ the reference on the same inputs:
   stream_triad             bench.py:93-99         a = b + alpha*c (numpy, two roundings)
   inclusive/exclusive scan algorithms.py:169-308  local accumulate, driver prefix, offset/seed
   black_scholes_call       bench.py:102-116       (scipy.special.erf, fp64 internals)
+  sort                     algorithms.py:315-432  sample sort (local sort, splitters, chunks)
 
 Pinning: tests/test_oracle.py checks every function here against golden vectors produced
 by the real reference (tests/golden/make_golden.py imports /root/reference and writes
@@ -200,6 +201,51 @@ def scan(x, p, out_dtype=None, exclusive=False, init=None, ufunc=np.add, threads
     _run([lambda k=k: fix(k) for k in live if exclusive or offsets[k] is not None], threads)
     out = np.concatenate(out_segs) if out_segs else np.empty(0, dtype=out_dtype)
     return out, partials
+
+
+def sample_sort(x, p, key=None, lengths=None):
+    """algorithms.py:315-432 (paper Alg. 5): local sort of every segment, n-1 evenly spaced
+    samples per segment, splitters from the pooled samples, redistribution into chunks by
+    searchsorted(splitters, key, side="left"), chunk sort, chunks swept back in order.
+    Returns the sorted copy of x (the reference sorts in place)."""
+    segs = [np.array(sg) for sg in block_segments(x, p, lengths)]
+    n_chunks = len(segs)
+    if len(x) <= 1 or n_chunks == 0:
+        return np.array(x)
+
+    def kv(a):
+        return a if key is None else key(a)
+
+    def local_sort(a):
+        if key is None:
+            a.sort()
+        else:
+            a[...] = a[np.argsort(kv(a), kind="stable")]
+
+    live = [sg for sg in segs if len(sg)]
+    for sg in live:
+        local_sort(sg)
+    if n_chunks == 1:
+        return segs[0]
+    samples = []
+    for sg in live:
+        m = len(sg)
+        samples.append(sg.copy() if m < n_chunks - 1 else sg[[(j + 1) * m // n_chunks for j in range(n_chunks - 1)]])
+    pool = np.concatenate(samples)
+    pool = pool[np.argsort(kv(pool), kind="stable")]
+    m = len(pool)
+    split_keys = kv(pool[[(j + 1) * m // n_chunks for j in range(n_chunks - 1)]])
+    chunks = [[] for _ in range(n_chunks)]
+    for sg in live:
+        idx = np.searchsorted(split_keys, kv(sg), side="left")
+        for j in range(n_chunks):
+            chunks[j].append(sg[idx == j])
+    out = []
+    for parts in chunks:
+        c = np.concatenate(parts) if parts else np.empty(0, dtype=x.dtype)
+        local_sort(c)
+        out.append(c)
+    return np.concatenate(out)
 
 
 def _pyop(ufunc):

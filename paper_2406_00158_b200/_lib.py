@@ -79,6 +79,7 @@ SIGNATURES = {
     "drk_sort_keys": (_int, [_int, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
     "drk_sort_pairs": (_int, [_int, _vp, _vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
     "drk_gather": (_int, [_int, _vp, _vp, _vp, _i64, _int, _vp]),
+    "drk_sort_bounds": (_int, [_int, _vp, _i64, _vp, _int, _vp, _int, _vp]),
     "drk_tune": (_int, [_cp, _int]),
     "drk_scan_set_trace": (_int, [_vp]),
     "drk_launch_count": (_i64, []),
@@ -154,6 +155,18 @@ def device_count() -> int:
 
 def launch_count() -> int:
     return int(load().drk_launch_count())
+
+
+# sort / gather / bounds also take unsigned keys (drk.h DRK_U32 / DRK_U64)
+SORT_DTYPE_CODE = {**DTYPE_CODE, np.dtype(np.uint32): 4, np.dtype(np.uint64): 5}
+
+
+def sort_dtype_code(dtype) -> int:
+    try:
+        return SORT_DTYPE_CODE[np.dtype(dtype)]
+    except KeyError:
+        raise TypeError(f"dtype {np.dtype(dtype)} cannot be sorted on the device "
+                        "(supported: float32, float64, int32, int64, uint32, uint64)") from None
 
 
 def dtype_code(dtype) -> int:

@@ -399,14 +399,16 @@ def _check_carry_range(op, partials, live, exclusive, init, T, carry=None):
 # sort
 
 
-def sort(r, key=None) -> None:
+def sort(r, key=None, *, strategy: str | None = None) -> None:
     """In-place ascending sort of a distributed vector (algorithms.py:315-432); with `key`,
     a stable sort by key(x) (the key function is traced like any element function).
 
-    The segments are gathered into one buffer on the first segment's GPU (peer copies over
-    NVLink for segments on other GPUs), radix-sorted there (CUB, library code: sort is not
-    on the benchmarked path) and written back in segment order.  A multi-GPU sample sort
-    with an all-to-all exchange is the scalable version of this."""
+    strategy "sample" (the default when the segments live on more than one GPU): the
+    reference's distributed sample sort — local sorts, splitters, redistribution into
+    per-locale chunks over NVLink, chunk sorts, sweep back (_sort.py).
+    strategy "gather" (the default on one GPU): the segments are concatenated in one buffer,
+    radix-sorted once and written back in segment order — one sort instead of two when
+    there is no second GPU to share the work.  Both give the reference's result."""
     from .containers import VectorSegment
     from .runtime import torch, torch_dtype
 
@@ -414,13 +416,24 @@ def sort(r, key=None) -> None:
     for s_ in segs:
         if not isinstance(s_, VectorSegment):
             raise TypeError("sort needs raw writable storage segments")
+    if strategy not in (None, "auto", "gather", "sample"):
+        raise ValueError(f"unknown sort strategy {strategy!r}")
     live = [s_ for s_ in segs if len(s_)]
     total = sum(len(s_) for s_ in live)
     if total <= 1:
         return
     rt = _require_runtime(runtime_of(r), "sort")
+    if len({s_.dtype for s_ in live}) > 1:
+        raise TypeError("sort needs segments of one dtype")
+    if strategy in (None, "auto"):
+        strategy = "sample" if len({rt.device_of(s_.rank) for s_ in live}) > 1 else "gather"
+    if strategy == "sample" and len(segs) > 1:
+        from ._sort import sample_sort
+
+        sample_sort(rt, segs, key)
+        return
     T = np.dtype(live[0].dtype)
-    code = _lib.dtype_code(T)
+    code = _lib.sort_dtype_code(T)
     states = {rt.state_of(s_.rank).index: rt.state_of(s_.rank) for s_ in live}
     from .runtime import await_pending
 
@@ -453,7 +466,7 @@ def sort(r, key=None) -> None:
         if node is None or isinstance(node, tuple):
             raise TypeError("sort key must return one value per element")
         K = np.dtype(node.dtype)
-        if K not in _lib.DTYPE_CODE:
+        if K not in _lib.SORT_DTYPE_CODE:
             node, K = expr.cast(node, np.int32 if K.kind == "b" else np.float64), np.dtype(
                 np.int32 if K.kind == "b" else np.float64)
         with t.cuda.stream(st0.stream):
@@ -464,11 +477,11 @@ def sort(r, key=None) -> None:
         tgt = _DeviceTarget(kbuf, K, st0.index)
         run_map([(tgt, node)], [kernels._TensorLeaf(buf, T, total)], total, launch)
         _lib.call("drk_iota", _lib.I64, idx.data_ptr(), total, 0, st0.index, st0.handle)
-        _lib.call("drk_sort_pairs", _lib.DTYPE_CODE[K], kbuf.data_ptr(), kalt.data_ptr(), idx.data_ptr(),
+        _lib.call("drk_sort_pairs", _lib.sort_dtype_code(K), kbuf.data_ptr(), kalt.data_ptr(), idx.data_ptr(),
                   idx_alt.data_ptr(), total, None, ctypes.byref(need), st0.index, st0.handle)
         with t.cuda.stream(st0.stream):
             scratch = t.empty(max(1, need.value), dtype=t.uint8, device=st0.device)
-        _lib.call("drk_sort_pairs", _lib.DTYPE_CODE[K], kbuf.data_ptr(), kalt.data_ptr(), idx.data_ptr(),
+        _lib.call("drk_sort_pairs", _lib.sort_dtype_code(K), kbuf.data_ptr(), kalt.data_ptr(), idx.data_ptr(),
                   idx_alt.data_ptr(), total, scratch.data_ptr(), ctypes.byref(need), st0.index, st0.handle)
         _lib.call("drk_gather", code, alt.data_ptr(), buf.data_ptr(), idx.data_ptr(), total, st0.index, st0.handle)
         result = alt

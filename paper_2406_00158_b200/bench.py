@@ -22,7 +22,7 @@ from .containers import DistributedVector
 from .runtime import Runtime
 from .views import get_zip_mode, set_zip_mode
 
-BENCH_NAMES = ("dot", "reduce", "inclusive_scan", "black_scholes", "stream")
+BENCH_NAMES = ("dot", "reduce", "inclusive_scan", "black_scholes", "stream", "sort")
 DEFAULT_SIZES = {name: 10**7 for name in BENCH_NAMES}
 REL_TOL = 1e-12
 STREAM_ALPHA = 3.0
@@ -173,9 +173,11 @@ def rel_close(actual, expected, tol) -> bool:
     return bool(np.isclose(np.asarray(actual), np.asarray(expected), rtol=tol, atol=0.0).all())
 
 
-def _timed(reps, kernel):
+def _timed(reps, kernel, reset=None):
     seconds, result = [], None
     for _ in range(reps):
+        if reset is not None:
+            reset()
         t0 = time.perf_counter()
         result = kernel()
         seconds.append(time.perf_counter() - t0)
@@ -261,7 +263,25 @@ def bench_stream(spec: BenchSpec, rt: Runtime) -> BenchResult:
     return res
 
 
+def bench_sort(spec: BenchSpec, rt: Runtime) -> BenchResult:
+    """Reference bench.py:332-345: sort splitmix64 uint64 keys, reset before every rep."""
+    n = spec.size
+    keys = repro.splitmix64(spec.seed, 0, n)
+    v = DistributedVector(rt, n, dtype=np.uint64)
+
+    def reset():
+        algorithms.copy(keys, v)
+
+    seconds, _ = _timed(spec.reps, lambda: algorithms.sort(v), reset=reset)
+    data = v.to_numpy()
+    res = BenchResult(spec, seconds, repro.checksum(data))
+    if spec.check:
+        res.verified = bool(np.array_equal(data, np.sort(keys)))
+    return res
+
+
 BENCHES = {
+    "sort": bench_sort,
     "dot": bench_dot,
     "reduce": bench_reduce,
     "inclusive_scan": bench_inclusive_scan,

@@ -205,6 +205,22 @@ def main():
         A.copy(v3, v4)
         add_case({"op": "copy", "dtype": dt, "n": n, "p": 4, "inputs": [d]}, v4.to_numpy())
 
+    # sort (algorithms.py:315-432): sample sort, optionally by a key function (stable)
+    sort_keys = {"none": None, "abs": np.abs, "neg": np.negative}
+    for dt in ("int32", "int64", "float32", "float64"):
+        for n in (0, 1, 2, 3, 5, 17, 1000, 4099):
+            for p in P:
+                for kname in ("none", "abs", "neg"):
+                    if kname != "none" and n not in (17, 4099):
+                        continue
+                    # ties on purpose (mod 41 around zero) so a key sort's stability shows
+                    d = ({"kind": "mod", "seed": 5, "start": 0, "n": n, "modulus": 41, "offset": -20}
+                         if kname != "none" or dt.startswith("int") else {"kind": "unit", "seed": 5, "start": 0, "n": n})
+                    x = gen(d, dt)
+                    v = DistributedVector.from_numpy(rts[p], x)
+                    A.sort(v, key=sort_keys[kname])
+                    add_case({"op": "sort", "dtype": dt, "n": n, "p": p, "key": kname, "inputs": [d]}, v.to_numpy())
+
     # reference known-answer tests (tests/test_bench.py, tests/test_algorithms.py)
     kat = {
         "dot_123_456": B.dot_product(DistributedVector.from_numpy(rts[3], np.array([1.0, 2.0, 3.0])),

@@ -533,6 +533,41 @@ class TestSort:
         sr.sort(v)
         assert np.array_equal(v.to_numpy(), np.sort(x))
 
+    @pytest.mark.parametrize("strategy", ["sample", "gather"])
+    def test_sample_sort_large(self, rt_pool, strategy):
+        # 8 locales on the visible GPU(s): local sorts, splitters, chunk exchange, sweep back
+        x = O.unit_doubles(7, 0, (1 << 22) + 13).astype(np.float32)
+        v = dvec(rt_pool(8), x, dtype=np.float32)
+        sr.sort(v, strategy=strategy)
+        assert np.array_equal(v.to_numpy(), np.sort(x))
+
+    @pytest.mark.parametrize("strategy", ["sample", "gather"])
+    def test_uint64_keys_like_reference_bench(self, rt_pool, strategy):
+        keys = O.splitmix64(1, 0, 100_003)
+        v = sr.DistributedVector(rt_pool(7), len(keys), dtype=np.uint64)
+        sr.copy(keys, v)
+        sr.sort(v, strategy=strategy)
+        assert np.array_equal(v.to_numpy(), np.sort(keys))
+
+    @pytest.mark.parametrize("strategy", ["sample", "gather"])
+    def test_key_sort_stable_large(self, rt_pool, strategy):
+        x = (O.mod_ints(3, 0, 300_001, 1001, -500)).astype(np.int64)
+        v = sr.DistributedVector.from_numpy(rt_pool(5), x)
+        sr.sort(v, key=lambda e: e % 17, strategy=strategy)
+        assert np.array_equal(v.to_numpy(), x[np.argsort(x % 17, kind="stable")])
+
+    def test_nan_sorts_last(self, rt_pool):
+        x = np.array([3.0, np.nan, -1.0, 2.0, np.nan, 0.5, -7.0, 1.0] * 50, dtype=np.float64)
+        for strategy in ("sample", "gather"):
+            v = sr.DistributedVector.from_numpy(rt_pool(4), x)
+            sr.sort(v, strategy=strategy)
+            got, exp = v.to_numpy(), np.sort(x)
+            assert np.array_equal(got, exp, equal_nan=True)
+
+    def test_unknown_strategy(self, rt3):
+        with pytest.raises(ValueError):
+            sr.sort(dvec(rt3, [2, 1]), strategy="bogus")
+
 
 class TestAsyncTransfers:
     def test_async_upload_then_compute(self, rt3):

@@ -19,7 +19,7 @@ def test_bad_reps_value(capsys):
     assert run(["--bench", "dot", "--reps", "0"]) == 2
 
 
-def test_gemm_and_sort_are_not_offered(capsys):
+def test_gemm_is_not_offered(capsys):
     assert run(["--bench", "gemm"]) == 2
 
 

@@ -151,3 +151,21 @@ def test_known_answers(rt3):
     assert abs(float(B.black_scholes_call(100.0, 100.0, 0.0, 0.2, 1.0)) - dec(kat["bs_atm"])) < 1e-12
     assert float(B.black_scholes_call(110.0, 100.0, 0.0, 0.0, 1.0)) == 10.0
     assert float(B.black_scholes_call(90.0, 100.0, 0.0, 0.0, 1.0)) == 0.0
+
+
+SORT_KEYS = {"none": None, "abs": lambda x: np.abs(x), "neg": lambda x: -x}
+
+
+@pytest.mark.parametrize("strategy", ["sample", "gather"])
+@_sel("sort")
+def test_sort(case, strategy, rt_pool, gold):
+    """Both sort strategies reproduce the reference's sample sort bit-for-bit (keys: the
+    stable order of equal keys is part of the result)."""
+    dt = np.dtype(case["dtype"])
+    x = O.generate(case["inputs"][0], dt)
+    v = _vec(rt_pool(case["p"]), x)
+    A.sort(v, key=SORT_KEYS[case["key"]], strategy=strategy)
+    got = v.to_numpy()
+    assert O.checksum(got) == case["checksum"]
+    if case.get("array"):
+        assert np.array_equal(got, gold.arrays[case["id"]])

@@ -9,6 +9,7 @@ from conftest import dec, golden
 from oracle import segrange_port as O
 
 CASES = golden().cases
+SORT_KEYS = {"none": None, "abs": np.abs, "neg": np.negative}
 
 
 def _ids(cases):
@@ -34,6 +35,8 @@ def _run(case):
         return None, O.black_scholes_prices(ins, dt, case["p"])
     if op == "copy":
         return None, ins[0].copy()
+    if op == "sort":
+        return None, O.sample_sort(ins[0], case["p"], SORT_KEYS[case["key"]])
     raise AssertionError(op)
 
 
