@@ -44,6 +44,10 @@ int drk_device_count(int* count);
 /* cudaMemcpyAsync with cudaMemcpyDefault (host<->device, device<->device, peer over NVLink) */
 int drk_memcpy_async(void* dst, const void* src, size_t bytes, int device, void* stream);
 int drk_memset_async(void* dst, int value, size_t bytes, int device, void* stream);
+/* copy `bytes` (multiple of 8) of device results into mapped pinned host memory with a
+ * one-CTA kernel instead of a copy engine, so the per-segment result readback of reduce /
+ * scan (algorithms.py:147-149, 256-262) never queues behind bulk downloads on other streams */
+int drk_readback(void* host_dst, const void* dev_src, size_t bytes, int device, void* stream);
 /* the wait_all barrier for one locale stream (runtime.py:229-245) */
 int drk_stream_synchronize(int device, void* stream);
 /* let kernels on `device` load/store memory of `peer` (NVLink P2P through NVSwitch) */

@@ -56,6 +56,31 @@ extern "C" int drk_memcpy_async(void* dst, const void* src, size_t bytes, int de
   return 0;
 }
 
+// Result readback through the SMs: a few 8-byte words stored straight into mapped pinned
+// host memory.  A cudaMemcpyAsync D2H of 8 bytes would queue on the copy engine behind any
+// multi-GB download in flight on another stream (bench.py e2e), stalling the compute stream.
+__global__ void readback_kernel(unsigned long long* __restrict__ dst, const unsigned long long* __restrict__ src,
+                                int words) {
+  for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+
+extern "C" int drk_readback(void* host_dst, const void* dev_src, size_t bytes, int device, void* stream) {
+  if (bytes == 0) return 0;
+  if (!host_dst || !dev_src) return set_error(DRK_E_ARG, "drk_readback: null pointer");
+  if (bytes % 8) return set_error(DRK_E_ARG, "drk_readback: bytes must be a multiple of 8");
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) DRK_CHECK(cudaSetDevice(device));
+  void* dptr = nullptr;
+  DRK_CHECK(cudaHostGetDevicePointer(&dptr, host_dst, 0));  // fails unless host_dst is mapped pinned memory
+  const int words = (int)(bytes / 8);
+  readback_kernel<<<1, words < 256 ? ((words + 31) / 32) * 32 : 256, 0, (cudaStream_t)stream>>>(
+      (unsigned long long*)dptr, (const unsigned long long*)dev_src, words);
+  g_launches.fetch_add(1);
+  DRK_CHECK(cudaGetLastError());
+  return 0;
+}
+
 extern "C" int drk_memset_async(void* dst, int value, size_t bytes, int device, void* stream) {
   if (bytes == 0) return 0;
   if (!dst) return set_error(DRK_E_ARG, "drk_memset_async: null pointer");
@@ -113,6 +138,7 @@ static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned
 static int g_scan_l2_min = 1 << 22;
 static int g_scan_l2_subs = 8;   // sub-tiles per L2 tile (160 KB for fp32)
 static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
+static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
 static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
                                  // measured slower than one 120 KB tile per CTA
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
@@ -140,6 +166,9 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2_ring")) {
     old = g_scan_l2_ring;
     g_scan_l2_ring = value;
+  } else if (!strcmp(name, "scan_debug")) {
+    old = g_scan_debug;
+    g_scan_debug = value;
   } else if (!strcmp(name, "scan_l2_pipe")) {
     old = g_scan_l2_pipe;
     g_scan_l2_pipe = value;
@@ -738,6 +767,7 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   p.epoch = next_epoch(scratch);
   p.bulk_ok = aligned16(in) && aligned16(out);
   p.trace = (u64*)g_scan_trace;
+  p.debug = g_scan_debug;
   cudaStream_t s = (cudaStream_t)stream;
   int rc = 0;
   switch (g_scan_sub) {

@@ -143,7 +143,9 @@ class DeviceState:
     def fetch_results(self, slots: int) -> np.ndarray:
         """Copy result slots [0, slots) to pinned host memory and wait (raw bytes)."""
         nbytes = slots * self.RESULT_BYTES
-        _lib.call("drk_memcpy_async", self._host_results.data_ptr(), self._results.data_ptr(), nbytes,
+        # stored by a kernel into mapped pinned memory: no copy engine, so this never waits
+        # behind a bulk download running on the d2h stream
+        _lib.call("drk_readback", self._host_results.data_ptr(), self._results.data_ptr(), nbytes,
                   self.index, self.handle)
         self.synchronize()
         return self._host_results.numpy()[:nbytes].copy()

@@ -5,9 +5,9 @@ algorithms.py:146-149 for reduce, :256-262 for the scan carry).  When the segmen
 vector are spread over processes — one process per B200, launched by torchrun — those
 two driver steps become collectives:
 
-  reduce:  each rank folds its own segments' device partials, then one NCCL all-reduce
-           of a single accumulator-typed element (float32 sums travel as float64,
-           int32 sums as int64, exactly like the device accumulators).
+  reduce:  each rank folds its own segments' device partials, then one NCCL all-gather
+           of (has, partial) pairs and the reference's ascending fold from init on every
+           rank (so the result does not depend on NCCL's reduction order).
   scan:    each rank computes its segment total on the device, one NCCL all-gather of
            (has, total) pairs, then rank r folds the totals of ranks < r into its carry
            and runs the single-pass device scan with that carry.  This is the
@@ -76,42 +76,70 @@ def _identity(opname, dtype):
     return dtype.type(info.max if opname == "minimum" else info.min)
 
 
-def allreduce_partial(partial, opname: str, acc_dtype, group: Group):
-    """Combine one accumulator-typed partial per rank (None = rank had no elements)."""
+def _encode(value, A):
+    """An accumulator/partial value as 8 raw bytes (float64 for floats, int64 for ints:
+    exact for every partial dtype of the device kernels)."""
+    wide = np.float64 if np.dtype(A).kind == "f" else np.int64
+    return np.array([value], dtype=wide).view(np.int64)[0]
+
+
+def _decode(bits, A):
+    wide = np.float64 if np.dtype(A).kind == "f" else np.int64
+    return np.asarray(np.array([bits], dtype=np.int64).view(wide)[0]).astype(A)[()]
+
+
+def gather_pairs(value, acc_dtype, group: Group, state=None) -> list:
+    """All-gather of one optional value per rank -> list indexed by rank (None = that rank
+    had no elements).  With NCCL the (has, value) pair is written by a kernel, gathered on
+    the rank's compute stream and read back by a kernel into mapped pinned memory: no
+    copy engine is involved, so the exchange never queues behind bulk PCIe transfers."""
     t = _torch()
     dist = _dist()
     A = np.dtype(acc_dtype)
-    val = _identity(opname, A) if partial is None else A.type(partial)
-    x = t.from_numpy(np.array([val], dtype=A)).to(group.device())
-    has = t.tensor([0 if partial is None else 1], dtype=t.int64, device=group.device())
-    dist.all_reduce(x, op=getattr(dist.ReduceOp, _REDUCE_OPS[opname]), group=group.group)
-    dist.all_reduce(has, op=dist.ReduceOp.SUM, group=group.group)
-    if int(has.item()) == 0:
-        return None
-    return x.cpu().numpy()[0]
+    pair = np.zeros(2, dtype=np.int64)
+    if value is not None:
+        pair[0], pair[1] = 1, _encode(value, A)
+    if group.backend == "nccl" and state is not None:
+        with t.cuda.stream(state.stream):
+            buf = t.empty(2, dtype=t.int64, device=state.device)
+            out = t.empty(2 * group.size, dtype=t.int64, device=state.device)
+        for k in range(2):
+            w = np.array([pair[k]], dtype=np.int64)
+            _lib.call("drk_fill", _lib.I64, buf.data_ptr() + 8 * k, 1, w.ctypes.data, state.index, state.handle)
+        with t.cuda.device(state.index), t.cuda.stream(state.stream):
+            dist.all_gather_into_tensor(out, buf, group=group.group)
+        host = t.empty(2 * group.size, dtype=t.int64, pin_memory=True)
+        _lib.call("drk_readback", host.data_ptr(), out.data_ptr(), 16 * group.size, state.index, state.handle)
+        state.synchronize()
+        got = host.numpy().reshape(group.size, 2)
+    else:
+        x = t.from_numpy(pair).to(group.device())
+        outs = t.empty(2 * group.size, dtype=t.int64, device=x.device)
+        dist.all_gather_into_tensor(outs, x, group=group.group)
+        got = outs.cpu().numpy().reshape(group.size, 2)
+    return [_decode(v, A) if h else None for h, v in got]
 
 
-def gather_totals(total, acc_dtype, group: Group) -> list:
+def allreduce_partial(partial, opname: str, acc_dtype, group: Group, state=None):
+    """Combine one partial per rank (None = rank had no elements), folded in rank order
+    like the reference's driver fold of segment partials (algorithms.py:147-149), so the
+    result does not depend on the collective's reduction order."""
+    fold = _PYOPS[opname]
+    acc = None
+    for q in gather_pairs(partial, acc_dtype, group, state):
+        if q is not None:
+            acc = q if acc is None else fold(acc, q)
+    return acc
+
+
+def gather_totals(total, acc_dtype, group: Group, state=None) -> list:
     """All-gather of per-rank (has, total) -> list indexed by rank (None = no elements)."""
-    t = _torch()
-    dist = _dist()
-    A = np.dtype(acc_dtype)
-    pair = np.zeros(2, dtype=np.float64 if A.kind == "f" else np.int64)
-    if total is not None:
-        pair[0], pair[1] = 1, total
-    x = t.from_numpy(pair).to(group.device())
-    out = [t.empty_like(x) for _ in range(group.size)]
-    dist.all_gather(out, x, group=group.group)
-    res = []
-    for o in out:
-        h, v = o.cpu().numpy()
-        res.append(A.type(v) if h else None)
-    return res
+    return gather_pairs(total, acc_dtype, group, state)
 
 
-def exclusive_carry(total, opname: str, acc_dtype, group: Group):
+def exclusive_carry(total, opname: str, acc_dtype, group: Group, state=None):
     """Fold of the totals of ranks before this one (None if all of them were empty)."""
-    totals = gather_totals(total, acc_dtype, group)
+    totals = gather_totals(total, acc_dtype, group, state)
     fold = _PYOPS[opname]
     carry = None
     for r in range(group.rank):
@@ -126,7 +154,10 @@ def exclusive_carry(total, opname: str, acc_dtype, group: Group):
 
 
 def reduce(local, init, op, group: Group):
-    """Global reduce of the concatenation of every rank's `local` range."""
+    """Global reduce of the concatenation of every rank's `local` range: the rank's device
+    partial, an all-gather of one partial per rank, then the reference's ascending driver
+    fold from `init` (algorithms.py:146-149) — bit-identical to the one-process result
+    when every rank holds one segment."""
     from . import algorithms as A
 
     op = A.as_binary_op(op)
@@ -143,13 +174,23 @@ def reduce(local, init, op, group: Group):
         for p in parts:
             partial = p if partial is None else op.fn(partial, p)
     code_dt = vdt if vdt is not None else np.dtype(getattr(local, "dtype", np.float64))
-    acc = _lib.acc_dtype(code_dt, A.OPCODES[opname]) if code_dt in _lib.DTYPE_CODE else code_dt
-    total = allreduce_partial(partial, opname, acc, group)
-    if total is None:
-        return init.item() if isinstance(init, np.generic) else init
-    L = A._partial_dtype(op, code_dt)
-    r = op.fn(init, np.asarray(total).astype(L)[()])
-    return r.item() if isinstance(r, np.generic) else r
+    L = A._partial_dtype(op, code_dt) if code_dt in _lib.DTYPE_CODE else code_dt
+    acc = init
+    for q in gather_pairs(partial, L, group, _state_of(rt, local)):
+        if q is not None:
+            acc = op.fn(acc, q)
+    return acc.item() if isinstance(acc, np.generic) else acc
+
+
+def _state_of(rt, local):
+    """The device state of the rank's (first) segment, if the runtime has devices."""
+    if rt is None or getattr(rt, "backend", None) != "cuda":
+        return None
+    from . import algorithms as A
+
+    segs = A.segments_of(local)
+    rank = next((s.rank for s in segs if getattr(s, "rank", None) is not None), 0)
+    return rt.state_of(rank)
 
 
 def inclusive_scan(local, out, group: Group, op=None):
@@ -175,5 +216,6 @@ def _scan(local, out, group, op, exclusive, init):
         rt = A.runtime_of(local)
         for p in A._segment_partials(rt, pieces, op):
             total = p if total is None else op.fn(total, p)
-    carry = exclusive_carry(None if total is None else acc.type(total), opname, acc, group)
+    st = _state_of(A.runtime_of(local), local) if pieces else None
+    carry = exclusive_carry(None if total is None else acc.type(total), opname, acc, group, st)
     return A._scan_impl(local, out, op, exclusive, init, carry=carry)

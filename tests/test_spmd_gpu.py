@@ -29,6 +29,17 @@ def test_spmd_three_ranks_one_gpu():
     assert out.stdout.count("'dot': True, 'scan': True, 'exscan': True, 'min': True") == 3
 
 
+def test_spmd_nccl_one_rank():
+    # the NCCL exchange itself (fill kernels -> all_gather_into_tensor on the compute stream
+    # -> kernel readback) on a world of one: the only NCCL world one GPU can host
+    env = dict(os.environ, SPMD_BACKEND="nccl")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "spmd_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "'dot': True, 'scan': True, 'exscan': True, 'min': True" in out.stdout
+
+
 def test_bench_two_ranks_shared_gpu():
     env = dict(os.environ, DRK_BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",

@@ -1,5 +1,7 @@
 """Multi-process check of the one-process-per-GPU path on a single GPU (gloo exchange,
-all ranks on GPU 0): distributed dot and scan of a global vector against numpy."""
+all ranks on GPU 0): distributed dot and scan of a global vector against numpy.
+SPMD_BACKEND=nccl (one rank) runs the NCCL exchange: kernel-built pairs, all-gather on the
+compute stream, kernel readback."""
 import os, sys
 import numpy as np
 import torch
@@ -9,9 +11,9 @@ import paper_2406_00158_b200 as sr
 from paper_2406_00158_b200 import algorithms as A, repro, spmd, views
 from oracle import segrange_port as O
 
-dist.init_process_group("gloo")
-rank, world = dist.get_rank(), dist.get_world_size()
 torch.cuda.set_device(0)
+dist.init_process_group(os.environ.get("SPMD_BACKEND", "gloo"), device_id=torch.device("cuda", 0) if os.environ.get("SPMD_BACKEND") == "nccl" else None)
+rank, world = dist.get_rank(), dist.get_world_size()
 g = spmd.Group()
 n = 1 << 20
 N = n * world
