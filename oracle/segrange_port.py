@@ -203,6 +203,26 @@ def scan(x, p, out_dtype=None, exclusive=False, init=None, ufunc=np.add, threads
     return out, partials
 
 
+def trimmed_lengths(lengths, f, l):
+    """views.py:271-292 trim_segments on segment lengths: window [f, l), no empty pieces."""
+    out, pos = [], 0
+    for n in lengths:
+        lo, hi = max(f, pos), min(l, pos + n)
+        if hi > lo:
+            out.append(hi - lo)
+        pos += n
+    return out
+
+
+def realigned_lengths(*length_lists):
+    """views.py:444-477 realign_segments: chunk lengths at the union of all boundaries."""
+    cuts = set()
+    for lst in length_lists:
+        cuts.update(np.cumsum([0] + list(lst)).tolist())
+    cuts = sorted(cuts)
+    return [b - a for a, b in zip(cuts, cuts[1:]) if b > a]
+
+
 def sample_sort(x, p, key=None, lengths=None):
     """algorithms.py:315-432 (paper Alg. 5): local sort of every segment, n-1 evenly spaced
     samples per segment, splitters from the pooled samples, redistribution into chunks by

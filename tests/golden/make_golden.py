@@ -221,6 +221,51 @@ def main():
                     A.sort(v, key=sort_keys[kname])
                     add_case({"op": "sort", "dtype": dt, "n": n, "p": p, "key": kname, "inputs": [d]}, v.to_numpy())
 
+    # view pipelines (views.py:271-556): reduce over drop|take, dot over a non-aligned zip,
+    # scan of a transform view, copy of a transform view
+    for dt, kind in (("int32", "mod"), ("float32", "unit"), ("float64", "unit")):
+        for n in (17, 1000, 4099):
+            for p in (1, 3, 4, 7):
+                for dr, tk in ((0, n), (3, n - 5), (n // 3, n // 2), (n - 1, 1)):
+                    d = ({"kind": "mod", "seed": 6, "start": 0, "n": n, "modulus": 2001, "offset": -1000}
+                         if kind == "mod" else {"kind": "unit", "seed": 6, "start": 0, "n": n})
+                    x = gen(d, dt)
+                    v = DistributedVector.from_numpy(rts[p], x)
+                    r = A.reduce(views.take(views.drop(v, dr), tk), 0, A.add)
+                    add_case({"op": "reduce_view", "dtype": dt, "n": n, "p": p, "drop": dr, "take": tk,
+                              "inputs": [d], "result": enc(r)})
+    for dt in ("float32", "float64"):
+        n = 1000
+        for pa, pb in (([500, 500], [300, 300, 400]), ([0, 1000], [999, 1]), ([250, 250, 250, 250], [1000])):
+            dx = {"kind": "unit", "seed": 7, "start": 0, "n": n}
+            dy = {"kind": "unit", "seed": 7, "start": n, "n": n}
+            x, y = gen(dx, dt), gen(dy, dt)
+            rt = rts[max(len(pa), len(pb))]
+            vx = DistributedVector.from_numpy(rt, x, partition=pa)
+            vy = DistributedVector.from_numpy(rt, y, partition=pb)
+            r = A.reduce(views.transform(views.zip(vx, vy), lambda t: t[0] * t[1]), 0.0, A.add)
+            add_case({"op": "dot_nonaligned", "dtype": dt, "n": n, "p": len(pa), "parts": [pa, pb],
+                      "inputs": [dx, dy], "result": enc(r)})
+    for n in (17, 1000, 4099):
+        for p in (1, 3, 7):
+            d = {"kind": "mod", "seed": 8, "start": 0, "n": n, "modulus": 2001, "offset": -1000}
+            x = gen(d, "int32")
+            v = DistributedVector.from_numpy(rts[p], x)
+            out = DistributedVector(rts[p], n, init=0, dtype=np.int32)
+            A.inclusive_scan(views.transform(v, lambda e: e * 3 - 1), out)
+            add_case({"op": "scan_view", "dtype": "int32", "n": n, "p": p, "inputs": [d]}, out.to_numpy())
+    for dt in ("float32", "float64", "int64"):
+        for n in (17, 4099):
+            for p in (1, 4):
+                d = ({"kind": "mod", "seed": 9, "start": 0, "n": n, "modulus": 2001, "offset": -1000}
+                     if dt == "int64" else {"kind": "unit", "seed": 9, "start": 0, "n": n})
+                x = gen(d, dt)
+                v = DistributedVector.from_numpy(rts[p], x)
+                out = DistributedVector(rts[p], n, init=0, dtype=np.dtype(dt))
+                A.copy(views.transform(v, lambda e: e * 2.5 + 1), out) if dt != "int64" else \
+                    A.copy(views.transform(v, lambda e: e * 7 - 3), out)
+                add_case({"op": "copy_transform", "dtype": dt, "n": n, "p": p, "inputs": [d]}, out.to_numpy())
+
     # reference known-answer tests (tests/test_bench.py, tests/test_algorithms.py)
     kat = {
         "dot_123_456": B.dot_product(DistributedVector.from_numpy(rts[3], np.array([1.0, 2.0, 3.0])),

@@ -16,6 +16,7 @@ from conftest import dec, golden
 import paper_2406_00158_b200 as sr
 from paper_2406_00158_b200 import algorithms as A
 from paper_2406_00158_b200 import bench as B
+from paper_2406_00158_b200 import views
 from paper_2406_00158_b200.algorithms import _scan_aligned
 from oracle import segrange_port as O
 
@@ -169,3 +170,52 @@ def test_sort(case, strategy, rt_pool, gold):
     assert O.checksum(got) == case["checksum"]
     if case.get("array"):
         assert np.array_equal(got, gold.arrays[case["id"]])
+
+
+@_sel("reduce_view")
+def test_reduce_over_drop_take(case, rt_pool):
+    dt = np.dtype(case["dtype"])
+    x = O.generate(case["inputs"][0], dt)
+    v = _vec(rt_pool(case["p"]), x)
+    got = A.reduce(views.take(views.drop(v, case["drop"]), case["take"]), 0, A.add)
+    exp = dec(case["result"])
+    if dt.kind == "i":
+        assert type(got) is type(exp) and got == exp
+    else:
+        assert _close(got, exp, case["dtype"]), (got, exp)
+
+
+@_sel("dot_nonaligned")
+def test_dot_over_nonaligned_zip(case, rt_pool):
+    dt = np.dtype(case["dtype"])
+    x, y = [O.generate(d, dt) for d in case["inputs"]]
+    pa, pb = case["parts"]
+    rt = rt_pool(max(len(pa), len(pb)))
+    vx = sr.DistributedVector.from_numpy(rt, x, partition=pa)
+    vy = sr.DistributedVector.from_numpy(rt, y, partition=pb)
+    got = A.reduce(views.transform(views.zip(vx, vy), lambda t: t[0] * t[1]), 0.0, A.add)
+    assert _close(got, dec(case["result"]), case["dtype"])
+
+
+@_sel("scan_view")
+def test_scan_of_transform_view(case, rt_pool, gold):
+    x = O.generate(case["inputs"][0], np.int32)
+    rt = rt_pool(case["p"])
+    out = sr.DistributedVector(rt, case["n"], init=0, dtype=np.int32)
+    A.inclusive_scan(views.transform(_vec(rt, x), lambda e: e * 3 - 1), out)
+    got = out.to_numpy()
+    assert O.checksum(got) == case["checksum"]
+    assert np.array_equal(got, gold.arrays[case["id"]])
+
+
+@_sel("copy_transform")
+def test_copy_of_transform_view(case, rt_pool, gold):
+    dt = np.dtype(case["dtype"])
+    x = O.generate(case["inputs"][0], dt)
+    rt = rt_pool(case["p"])
+    out = sr.DistributedVector(rt, case["n"], init=0, dtype=dt)
+    fn = (lambda e: e * 7 - 3) if dt.kind == "i" else (lambda e: e * 2.5 + 1)
+    A.copy(views.transform(_vec(rt, x), fn), out)
+    got = out.to_numpy()  # bit-exact: numpy's rounding of each operation (no FMA contraction)
+    assert O.checksum(got) == case["checksum"]
+    assert np.array_equal(got, gold.arrays[case["id"]])

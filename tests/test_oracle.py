@@ -35,6 +35,19 @@ def _run(case):
         return None, O.black_scholes_prices(ins, dt, case["p"])
     if op == "copy":
         return None, ins[0].copy()
+    if op == "reduce_view":
+        n, p = case["n"], case["p"]
+        lens = O.trimmed_lengths(O.block_lengths(n, p), case["drop"], case["drop"] + case["take"])
+        x = ins[0][case["drop"]: case["drop"] + case["take"]]
+        return O.reduce(x, len(lens), 0, np.add, lengths=lens), None
+    if op == "dot_nonaligned":
+        lens = O.realigned_lengths(*case["parts"])
+        return O.reduce(ins[0] * ins[1], len(lens), 0.0, np.add, lengths=lens), None
+    if op == "scan_view":
+        out, _ = O.scan(ins[0] * 3 - 1, case["p"], dt)
+        return None, out
+    if op == "copy_transform":
+        return None, (ins[0] * 7 - 3) if dt.kind == "i" else (ins[0] * 2.5 + 1)
     if op == "sort":
         return None, O.sample_sort(ins[0], case["p"], SORT_KEYS[case["key"]])
     raise AssertionError(op)

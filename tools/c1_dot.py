@@ -38,3 +38,12 @@ print(json.dumps({"config": "C1 dot fp32 n=2^24 P=2 (both segments on GPU 0)", "
                   "GB/s_api": round(8 * n / (api_us * 1e-6) / 1e9, 1),
                   "GB/s_kernels": round(8 * n / (2 * kern_us * 1e-6) / 1e9, 1),
                   "cpu_port_ms": round(cpu_ms, 2)}))
+
+if os.environ.get("C1_PROFILE"):
+    import cProfile, pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(200):
+        B.dot_product(vx, vy)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
