@@ -450,6 +450,40 @@ class TestJitExpressions:
         B.black_scholes_prices(out, *vecs)
         np.testing.assert_allclose(out.to_numpy(), O.black_scholes(*cols), rtol=1e-12)
 
+    @pytest.mark.parametrize("traced", [False, True])
+    def test_black_scholes_fp32_accuracy_large(self, rt_pool, traced):
+        # fp32 tier: 2^22 options over BS_RANGES against the reference's fp64-internal
+        # formula, rel <= 1e-5 everywhere (the SFU/erfc chain of BSMath<float>); traced=True
+        # goes through the NVRTC path (a lambda calling black_scholes_call + a no-op scale)
+        n = (1 << 22) + 7
+        cols = [O.uniform_doubles(11, k * n, n, lo, hi).astype(np.float32)
+                for k, (lo, hi) in enumerate(B.BS_RANGES.values())]
+        rt = rt_pool(3)
+        vecs = [dvec(rt, c, dtype=np.float32) for c in cols]
+        out = sr.DistributedVector(rt, n, dtype=np.float32)
+        if traced:
+            sr.for_each(views.zip(out, *vecs),
+                        lambda t: (B.black_scholes_call(t[1], t[2], t[3], t[4], t[5]) * 1.0,) + (None,) * 5)
+        else:
+            B.black_scholes_prices(out, *vecs)
+        got = out.to_numpy().astype(np.float64)
+        ref = O.black_scholes(*[c.astype(np.float64) for c in cols])
+        rel = np.abs(got - ref) / np.abs(ref)
+        assert rel.max() <= 1e-5, rel.max()
+
+    def test_black_scholes_fp32_edges(self, rt_pool):
+        # degenerate volatility/expiry -> discounted intrinsic value; deep in/out of the money
+        S = np.array([100, 100, 100, 100, 50, 200, 100, 100], dtype=np.float32)
+        K = np.array([90, 110, 90, 100, 100, 100, 100, 100], dtype=np.float32)
+        r = np.array([0.05, 0.05, 0.0, 0.01, 0.02, 0.02, 0.03, 0.03], dtype=np.float32)
+        v = np.array([0.0, 0.0, -0.2, 0.2, 0.2, 0.2, 2.0, 0.01], dtype=np.float32)
+        T = np.array([1.0, 1.0, 1.0, 0.0, 1.0, 1.0, 5.0, 0.01], dtype=np.float32)
+        rt = rt_pool(2)
+        out = sr.DistributedVector(rt, len(S), dtype=np.float32)
+        B.black_scholes_prices(out, *[dvec(rt, c, dtype=np.float32) for c in (S, K, r, v, T)])
+        ref = O.black_scholes(*[c.astype(np.float64) for c in (S, K, r, v, T)])
+        np.testing.assert_allclose(out.to_numpy(), ref, rtol=1e-5, atol=1e-5)
+
 
 class TestRuntime:
     def test_submit_and_wait_all(self, rt3):
