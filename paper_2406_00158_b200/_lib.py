@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdrk.so")
+LIB_PATH = os.environ.get("DRK_LIB") or os.path.join(_HERE, "libdrk.so")  # DRK_LIB: kernel experiments
 CSRC_DIR = os.path.join(_HERE, "csrc")
 
 # dtype codes (include/drk.h)
