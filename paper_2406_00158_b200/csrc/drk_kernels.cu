@@ -713,6 +713,7 @@ template <class T, class Op>
 static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int IT = ScanItems<T, Op>::value;
   switch (g_scan_l2_subs) {
+    case 7: return launch_scan_l2dyn<T, Op, 7, IT, 3>(p, n, s);
     case 6: return launch_scan_l2dyn<T, Op, 6, IT, 3>(p, n, s);
     case 10: return launch_scan_l2dyn<T, Op, 10, IT, 3>(p, n, s);
     case 12: return launch_scan_l2dyn<T, Op, 12, IT, 3>(p, n, s);
