@@ -136,7 +136,8 @@ static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
 static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
 static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned segments
 static int g_scan_l2_min = 1 << 22;
-static int g_scan_l2_subs = 8;   // sub-tiles per L2 tile (160 KB for fp32)
+static int g_scan_l2_subs = 0;   // sub-tiles per L2 tile (0: 8 = 160 KB for fp32, 7 for int32 sums)
+static int g_scan_l2_pre = 2;    // sub-tiles scanned prefix-free during the look-back
 static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
 static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
 static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
@@ -166,6 +167,9 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2_ring")) {
     old = g_scan_l2_ring;
     g_scan_l2_ring = value;
+  } else if (!strcmp(name, "scan_l2_pre")) {
+    old = g_scan_l2_pre;
+    g_scan_l2_pre = value;
   } else if (!strcmp(name, "scan_debug")) {
     old = g_scan_debug;
     g_scan_debug = value;
@@ -712,7 +716,11 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
 template <class T, class Op>
 static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int IT = ScanItems<T, Op>::value;
-  switch (g_scan_l2_subs) {
+  // int32 sums keep 12-element runs of int64 partials (96 KB at 8 sub-tiles); measured best
+  // at 7 sub-tiles, every other type at 8
+  const int subs = g_scan_l2_subs ? g_scan_l2_subs : (sizeof(T) == 4 && IT == 12 ? 7 : 8);
+  p.pre = g_scan_l2_pre;
+  switch (subs) {
     case 7: return launch_scan_l2dyn<T, Op, 7, IT, 3>(p, n, s);
     case 6: return launch_scan_l2dyn<T, Op, 6, IT, 3>(p, n, s);
     case 10: return launch_scan_l2dyn<T, Op, 10, IT, 3>(p, n, s);
