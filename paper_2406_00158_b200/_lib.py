@@ -125,6 +125,10 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        # DRK_TUNE="name=value,...": launch-parameter overrides for kernel experiments
+        for kv in filter(None, os.environ.get("DRK_TUNE", "").split(",")):
+            k, v = kv.split("=")
+            lib.drk_tune(k.strip().encode(), int(v))
         _lib = lib
         return lib
 
