@@ -48,6 +48,9 @@ int drk_memset_async(void* dst, int value, size_t bytes, int device, void* strea
  * one-CTA kernel instead of a copy engine, so the per-segment result readback of reduce /
  * scan (algorithms.py:147-149, 256-262) never queues behind bulk downloads on other streams */
 int drk_readback(void* host_dst, const void* dev_src, size_t bytes, int device, void* stream);
+/* device address of mapped pinned host memory (cudaHostGetDevicePointer): reductions store
+ * their per-segment result there directly, so reading it costs one stream sync */
+int drk_mapped_ptr(const void* host, void** dev);
 /* the wait_all barrier for one locale stream (runtime.py:229-245) */
 int drk_stream_synchronize(int device, void* stream);
 /* let kernels on `device` load/store memory of `peer` (NVLink P2P through NVSwitch) */

@@ -61,6 +61,7 @@ SIGNATURES = {
     "drk_memcpy_async": (_int, [_vp, _vp, _sz, _int, _vp]),
     "drk_memset_async": (_int, [_vp, _int, _sz, _int, _vp]),
     "drk_readback": (_int, [_vp, _vp, _sz, _int, _vp]),
+    "drk_mapped_ptr": (_int, [_vp, ctypes.POINTER(_vp)]),
     "drk_stream_synchronize": (_int, [_int, _vp]),
     "drk_enable_peer_access": (_int, [_int, _int]),
     "drk_copy": (_int, [_int, _vp, _vp, _i64, _int, _vp]),

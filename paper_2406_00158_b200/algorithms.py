@@ -212,7 +212,7 @@ def _segment_partials(rt, pieces, op):
         node = lw.value if opcode is not None else _promote_python(lw.value)
         run_reduce(node, lw.leaves, lw.length, opcode, combiner, launch, slot)
         order.append((st, slot, node.dtype))
-    raw = {id(l.state): l.state.fetch_results(slots[id(l.state)]) for l in launches.values()}
+    raw = {id(l.state): l.state.fetch_host_results(slots[id(l.state)]) for l in launches.values()}
     out = []
     for st, slot, vdt in order:
         if opcode is not None:
@@ -342,8 +342,8 @@ def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
         slot = per_dev_slot.get(id(st), 0)
         per_dev_slot[id(st)] = slot + 1
         kernels.launch_kernel("drk_reduce", launch, tgt.length, _lib.dtype_code(T), opcode, in_ptr, tgt.length,
-                       st.result_dev_ptr(slot), st.reduce_scratch.data_ptr())
-    fetched = {id(w[1]): w[1].fetch_results(per_dev_slot[id(w[1])]) for w in work}
+                       st.host_result_dev_ptr(slot), st.reduce_scratch.data_ptr())
+    fetched = {id(w[1]): w[1].fetch_host_results(per_dev_slot[id(w[1])]) for w in work}
     counter = {}
     for k, st, *_ in work:
         slot = counter.get(id(st), 0)

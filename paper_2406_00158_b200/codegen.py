@@ -506,7 +506,7 @@ def run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot):
     vec_ok = all(ptrs[k] % 16 == 0 for k in array_slots)
     st = launch.state
     scratch = st.reduce_scratch.data_ptr()
-    res = st.result_dev_ptr(slot)
+    res = st.host_result_dev_ptr(slot)
     blob = (words.pack() + struct.pack("<qi4x", n, 1 if vec_ok else 0)
             + struct.pack("<QQQ", scratch, scratch + 128, scratch + 128 + 4096 * 8)
             + struct.pack("<QQ", res, 0))

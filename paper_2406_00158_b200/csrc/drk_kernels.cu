@@ -81,6 +81,12 @@ extern "C" int drk_readback(void* host_dst, const void* dev_src, size_t bytes, i
   return 0;
 }
 
+extern "C" int drk_mapped_ptr(const void* host, void** dev) {
+  if (!host || !dev) return set_error(DRK_E_ARG, "drk_mapped_ptr: null pointer");
+  DRK_CHECK(cudaHostGetDevicePointer(dev, const_cast<void*>(host), 0));
+  return 0;
+}
+
 extern "C" int drk_memset_async(void* dst, int value, size_t bytes, int device, void* stream) {
   if (bytes == 0) return 0;
   if (!dst) return set_error(DRK_E_ARG, "drk_memset_async: null pointer");

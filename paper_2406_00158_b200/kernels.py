@@ -246,11 +246,11 @@ class _TensorLeaf(Leaf):
 
 
 def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
-    """Reduce `node` over n elements into result slot `slot` of launch.state (value in
-    drk_acc_dtype(node.dtype, op) for catalogue ops)."""
+    """Reduce `node` over n elements into host result slot `slot` of launch.state (value in
+    drk_acc_dtype(node.dtype, op) for catalogue ops; read with fetch_host_results)."""
     ptrs = stage_leaves(leaves, launch)
     st = launch.state
-    res = st.result_dev_ptr(slot)
+    res = st.host_result_dev_ptr(slot)  # stored straight into mapped pinned memory
     T = node.dtype
     if opcode is not None and T in _lib.DTYPE_CODE:
         code = _lib.DTYPE_CODE[T]

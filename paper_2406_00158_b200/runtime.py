@@ -18,6 +18,7 @@ logic can be exercised on machines without a GPU; it never computes.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import threading
 import weakref
@@ -132,6 +133,9 @@ class DeviceState:
         with t.cuda.stream(self.stream):
             self._results = t.zeros(slots * self.RESULT_BYTES, dtype=t.uint8, device=self.device)
         self._host_results = t.zeros(slots * self.RESULT_BYTES, dtype=t.uint8, pin_memory=True)
+        dev = ctypes.c_void_p()
+        _lib.call("drk_mapped_ptr", self._host_results.data_ptr(), ctypes.byref(dev))
+        self._host_results_dev = int(dev.value)
         self._result_slots = slots
 
     def result_ptr(self, slot: int) -> int:
@@ -139,6 +143,16 @@ class DeviceState:
 
     def result_dev_ptr(self, slot: int) -> int:
         return self.result_ptr(slot)
+
+    def host_result_dev_ptr(self, slot: int) -> int:
+        """Device address of host result slot `slot` (mapped pinned memory): reductions
+        store their result there directly (fetch with fetch_host_results)."""
+        return self._host_results_dev + slot * self.RESULT_BYTES
+
+    def fetch_host_results(self, slots: int) -> np.ndarray:
+        """Wait for the stream, then the raw bytes of host result slots [0, slots)."""
+        self.synchronize()
+        return self._host_results.numpy()[: slots * self.RESULT_BYTES].copy()
 
     def fetch_results(self, slots: int) -> np.ndarray:
         """Copy result slots [0, slots) to pinned host memory and wait (raw bytes)."""
