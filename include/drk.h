@@ -123,6 +123,18 @@ int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_
              void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
              int device, void* stream);
 
+/* Cross-segment scan carry on the device (algorithms.py:256-262, the driver's fold of segment
+ * totals): carry_out = carry_in ⊕ L(total_0) ⊕ ... ⊕ L(total_{count-1}) in the accumulator
+ * type of drk_acc_dtype(dtype, op), skipping totals whose int64 has-flag is 0 (has may be
+ * NULL).  totals / has are arrays of device addresses — peer memory of the GPUs that reduced
+ * them, or an all-gathered buffer.  carry_in is a host value (carry_in_host) and/or an earlier
+ * fold on the device (carry_in_dev, not re-rounded); either may be NULL.  With nothing to
+ * fold the fold's identity is written.  count <= DRK_CARRY_MAX. */
+#define DRK_CARRY_MAX 64
+int drk_carry_fold(int dtype, int op, const void* const* totals, const void* const* has, int count,
+                   const void* carry_in_host, const void* carry_in_dev, void* carry_out_dev, int device,
+                   void* stream);
+
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
  * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),
  * plus the splitter search of the distributed sample sort; the runtime moves the runs

@@ -261,9 +261,14 @@ def _scan_aligned(r, out, op, exclusive, init) -> list:
     return _scan_impl(r, out, op, exclusive, init)
 
 
-def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
+def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list:
     """Aligned scan with an optional incoming carry (the fold of everything before r,
-    in the accumulator type; used when r is one rank's block of a larger vector)."""
+    in the accumulator type; used when r is one rank's block of a larger vector).
+
+    carry_hook(total_ptrs, state) -> (carry_dev_ptr or None, carry_host_fn): the incoming
+    carry produced on the device between the two passes of the multi-device schedule (the
+    one-process-per-GPU scan, spmd.py); carry_host_fn() gives its value on the host after
+    the scan (for the int32 range check)."""
     op = as_binary_op(op)
     in_segs = segments_of(r)
     out_segs = segments_of(out)
@@ -311,7 +316,7 @@ def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
     if exclusive:
         init_a = _to_acc(init, A)
 
-    if len(devices) == 1:
+    if len(devices) == 1 and not _FORCE_MULTI_DEVICE_SCAN and carry_hook is None:
         # single device: chain the carry on the device, one pass per segment
         st = work[0][1]
         st.ensure_results(2 * len(work) + 2)
@@ -330,8 +335,12 @@ def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
         _check_carry_range(op, partials, live, exclusive, init, T, carry)
         return partials
 
-    # several devices: totals first (all GPUs in parallel), carries on the host exactly as
-    # the reference's driver loop, then one carried scan per segment.
+    if carry_hook is not None or (len(work) <= _lib.CARRY_MAX + 1 and not _FORCE_HOST_CARRY):
+        return _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, init, init_a, carry,
+                                  launches, carry_hook)
+    # several devices, host carry (more segments than drk_carry_fold takes): totals first
+    # (all GPUs in parallel), carries on the host exactly as the reference's driver loop,
+    # then one carried scan per segment.
     per_dev_slot = {}
     for k, st, launch, in_ptr, tgt in work:
         per_dev_slot[id(st)] = per_dev_slot.get(id(st), 0) + 1
@@ -358,6 +367,94 @@ def _scan_impl(r, out, op, exclusive, init, carry=None) -> list:
                  carry_value=_to_acc(off, A) if off is not None else None)
     for l in launches.values():
         l.state.synchronize()
+    return partials
+
+
+# Test hooks: take the multi-device scan schedule even when every segment shares one GPU
+# (_FORCE_MULTI_DEVICE_SCAN), or fold its carries on the host (_FORCE_HOST_CARRY).
+_FORCE_MULTI_DEVICE_SCAN = False
+_FORCE_HOST_CARRY = False
+
+
+def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, init, init_a, carry, launches,
+                       carry_hook=None):
+    """Scan of segments spread over several GPUs with the carry folded on the devices.
+
+    1. Every segment's total is reduced on its own GPU (all GPUs in parallel).
+    2. Each segment's stream waits (CUDA events) for the GPUs that hold earlier segments,
+       folds their totals straight from peer memory over NVLink (drk_carry_fold: the
+       reference's driver loop, algorithms.py:256-262, on the device), and scans with it.
+    The host reads the totals only afterwards (the white-box partials, the int32 carry
+    range check), so nothing between the two passes waits for the host."""
+    from .runtime import torch
+
+    t = torch()
+    code = _lib.dtype_code(T)
+    count = {}
+    for k, st, *_ in work:
+        count[id(st)] = count.get(id(st), 0) + 1
+    for k, st, *_ in work:
+        st.ensure_results(2 * count[id(st)])  # totals, then carries
+    tot_ptr, used = {}, {}
+    for k, st, launch, in_ptr, tgt in work:
+        slot = used.get(id(st), 0)
+        used[id(st)] = slot + 1
+        tot_ptr[k] = st.result_dev_ptr(slot)
+        kernels.launch_kernel("drk_reduce", launch, tgt.length, code, opcode, in_ptr, tgt.length, tot_ptr[k],
+                              st.reduce_scratch.data_ptr())
+    reduced = {}
+    for k, st, *_ in work:
+        if id(st) not in reduced:
+            ev = t.cuda.Event()
+            ev.record(st.stream)
+            reduced[id(st)] = ev
+    in_dev, carry_host_fn = None, None
+    if carry_hook is not None:
+        st0 = work[0][1]
+        for k, st, *_ in work:
+            if st is not st0:
+                st0.stream.wait_event(reduced[id(st)])
+        in_dev, carry_host_fn = carry_hook([tot_ptr[w[0]] for w in work], st0)
+        if any(w[1] is not st0 for w in work):
+            ev = t.cuda.Event()
+            ev.record(st0.stream)
+            for k, st, *_ in work:
+                if st is not st0:
+                    st.stream.wait_event(ev)
+    carry_buf = _lib.scalar_buffer(carry, A) if carry is not None else None
+    waited, carries = set(), {}
+    for i, (k, st, launch, in_ptr, tgt) in enumerate(work):
+        before = [w[0] for w in work[:i]]
+        for _, st2, *_rest in work[:i]:
+            if st2 is not st and (id(st), id(st2)) not in waited:
+                st.stream.wait_event(reduced[id(st2)])
+                waited.add((id(st), id(st2)))
+        carry_dev = None
+        if not before and carry_buf is None and in_dev is not None:
+            carry_dev = in_dev
+        elif before or carry_buf is not None:
+            cslot = count[id(st)] + carries.get(id(st), 0)
+            carries[id(st)] = carries.get(id(st), 0) + 1
+            vals = (ctypes.c_void_p * max(1, len(before)))(*[tot_ptr[j] for j in before])
+            carry_dev = st.result_dev_ptr(cslot)
+            kernels.launch_kernel("drk_carry_fold", launch, 1, code, opcode, vals, None, len(before),
+                                  ctypes.addressof(carry_buf) if carry_buf is not None else None, in_dev, carry_dev)
+        run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a, carry_dev=carry_dev)
+    raw = {}
+    for k, st, *_ in work:
+        if id(st) not in raw:
+            raw[id(st)] = st.fetch_results(count[id(st)])  # waits for the device's scans too
+    seen = {}
+    for k, st, *_ in work:
+        slot = seen.get(id(st), 0)
+        seen[id(st)] = slot + 1
+        total = np.frombuffer(raw[id(st)][8 * slot : 8 * slot + A.itemsize].tobytes(), dtype=A)[0]
+        partials[k] = total.astype(L).item()
+    for l in launches.values():
+        l.state.synchronize()
+    if carry_host_fn is not None:
+        carry = carry_host_fn()
+    _check_carry_range(op, partials, live, exclusive, init, T, carry)
     return partials
 
 

@@ -846,6 +846,100 @@ extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* 
 }
 
 // ---------------------------------------------------------------------------------------
+// cross-segment carry on the device (reference algorithms.py:256-262, the driver's fold of
+// segment totals).  A segment's GPU folds the totals of the segments before it straight from
+// where they were reduced (peer memory over NVLink, or an all-gathered buffer), so the scan
+// of a vector spread over several GPUs needs no host round trip between its two passes.
+
+// identity of the fold, used only when nothing precedes a segment: -0.0 for float sums
+// (x + -0.0 == x bit-for-bit, including x = -0.0), 1 for products, +-inf / int limits for
+// minimum / maximum
+template <class Op, class A> struct FoldIdent;
+template <class A> struct FoldIdent<OpAdd, A> {
+  static __device__ A v() { return is_float<A>::value ? (A)(-0.0) : (A)0; }
+};
+template <class A> struct FoldIdent<OpMul, A> {
+  static __device__ A v() { return (A)1; }
+};
+template <class A> struct FoldIdent<OpMin, A> {
+  static __device__ A v() {
+    if (is_float<A>::value) return (A)__longlong_as_double(0x7ff0000000000000ll);
+    return sizeof(A) == 4 ? (A)0x7fffffff : (A)0x7fffffffffffffffll;
+  }
+};
+template <class A> struct FoldIdent<OpMax, A> {
+  static __device__ A v() {
+    if (is_float<A>::value) return (A)__longlong_as_double((long long)0xfff0000000000000ull);
+    return sizeof(A) == 4 ? (A)(-0x7fffffff - 1) : (A)(-0x7fffffffffffffffll - 1);
+  }
+};
+
+struct CarryArgs {
+  const void* val[DRK_CARRY_MAX];
+  const long long* has[DRK_CARRY_MAX];
+};
+
+template <class T, class Op>
+__global__ void carry_fold_kernel(const CarryArgs a, int count, int has_in, typename WideAcc<T, Op>::type carry_in,
+                                  const typename WideAcc<T, Op>::type* carry_in_dev,
+                                  typename WideAcc<T, Op>::type* out) {
+  typedef typename LocalAcc<T, Op>::type L;
+  typedef typename WideAcc<T, Op>::type A;
+  Opt<A> acc;
+  acc.has = has_in;
+  acc.v = carry_in;
+  if (carry_in_dev) {  // an earlier fold: already in the accumulator type
+    Opt<A> c;
+    c.has = 1;
+    c.v = *carry_in_dev;
+    acc = opt_combine<Op>(acc, c);
+  }
+  for (int j = 0; j < count; ++j) {
+    if (a.has[j] && *a.has[j] == 0) continue;
+    Opt<A> v;
+    v.has = 1;
+    v.v = (A)(L) * (const A*)a.val[j];  // the reference folds the segment totals in numpy's dtype
+    acc = opt_combine<Op>(acc, v);
+  }
+  *out = acc.has ? acc.v : FoldIdent<Op, A>::v();
+}
+
+template <class T, class Op>
+static int carry_fold_t(const CarryArgs& a, int count, const void* carry_in_host, const void* carry_in_dev, void* out,
+                        int device, void* stream) {
+  typedef typename WideAcc<T, Op>::type A;
+  if (int rc = prologue(device, "drk_carry_fold")) return rc;
+  A cin = A();
+  if (carry_in_host) memcpy(&cin, carry_in_host, sizeof(A));
+  carry_fold_kernel<T, Op><<<1, 1, 0, (cudaStream_t)stream>>>(a, count, carry_in_host != nullptr, cin,
+                                                               (const A*)carry_in_dev, (A*)out);
+  return epilogue("drk_carry_fold");
+}
+
+extern "C" int drk_carry_fold(int dtype, int op, const void* const* totals, const void* const* has, int count,
+                              const void* carry_in_host, const void* carry_in_dev, void* carry_out_dev, int device,
+                              void* stream) {
+  if (count < 0 || count > DRK_CARRY_MAX) return set_error(DRK_E_ARG, "drk_carry_fold: count out of range");
+  if (!carry_out_dev || (count > 0 && !totals)) return set_error(DRK_E_ARG, "drk_carry_fold: null pointer");
+  CarryArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int j = 0; j < count; ++j) {
+    if (!totals[j]) return set_error(DRK_E_ARG, "drk_carry_fold: null total pointer");
+    a.val[j] = totals[j];
+    a.has[j] = has ? (const long long*)has[j] : nullptr;
+  }
+  DRK_DISPATCH(dtype, "drk_carry_fold", T, {
+    switch (op) {
+      case DRK_ADD: return carry_fold_t<T, OpAdd>(a, count, carry_in_host, carry_in_dev, carry_out_dev, device, stream);
+      case DRK_MUL: return carry_fold_t<T, OpMul>(a, count, carry_in_host, carry_in_dev, carry_out_dev, device, stream);
+      case DRK_MIN: return carry_fold_t<T, OpMin>(a, count, carry_in_host, carry_in_dev, carry_out_dev, device, stream);
+      case DRK_MAX: return carry_fold_t<T, OpMax>(a, count, carry_in_host, carry_in_dev, carry_out_dev, device, stream);
+    }
+    return set_error(DRK_E_ARG, "drk_carry_fold: unknown op");
+  });
+}
+
+// ---------------------------------------------------------------------------------------
 // scans of NVRTC-compiled kernels (custom associative operators)
 
 extern "C" int drk_jit_launch(void* handle, const char* kernel, unsigned grid, unsigned block, unsigned smem,

@@ -209,13 +209,72 @@ def _scan(local, out, group, op, exclusive, init):
     if opname not in _REDUCE_OPS:
         raise TypeError("distributed scan needs add/multiply/minimum/maximum")
     T = np.dtype(out.dtype)
-    acc = _lib.acc_dtype(T, A.OPCODES[opname])
+    opcode = A.OPCODES[opname]
+    acc = _lib.acc_dtype(T, opcode)
     pieces = A._pieces(local)
+    st = _state_of(A.runtime_of(local), local) if pieces else None
+    if pieces and st is not None and group.backend == "nccl" and group.size <= _lib.CARRY_MAX:
+        # device path: local totals -> (has, total) pair -> all-gather -> carry, all on the
+        # rank's stream; the host only checks the int32 carry range after the scan
+        return A._scan_impl(local, out, op, exclusive, init,
+                            carry_hook=_device_carry_hook(group, _lib.dtype_code(T), opcode, opname, acc))
     total = None
     if pieces:
         rt = A.runtime_of(local)
         for p in A._segment_partials(rt, pieces, op):
             total = p if total is None else op.fn(total, p)
-    st = _state_of(A.runtime_of(local), local) if pieces else None
     carry = exclusive_carry(None if total is None else acc.type(total), opname, acc, group, st)
     return A._scan_impl(local, out, op, exclusive, init, carry=carry)
+
+
+def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
+    """carry_hook for algorithms._scan_impl: between the scan's two passes, fold the rank's
+    segment totals into a (has, total) pair (drk_carry_fold), all-gather the pairs with NCCL
+    on the rank's stream, and fold the totals of lower ranks into the carry (drk_carry_fold
+    again) — no host round trip.  Returns (carry device pointer or None, host-value function)."""
+    import ctypes
+
+    t = _torch()
+    dist = _dist()
+    A = np.dtype(acc)
+
+    def hook(total_ptrs, st):
+        with t.cuda.stream(st.stream):
+            pair = t.zeros(2, dtype=t.int64, device=st.device)
+            gathered = t.empty(2 * group.size, dtype=t.int64, device=st.device)
+            carry = t.zeros(1, dtype=t.int64, device=st.device)
+        one = np.array([1], dtype=np.int64)
+        _lib.call("drk_fill", _lib.I64, pair.data_ptr(), 1, one.ctypes.data, st.index, st.handle)
+        vals = (ctypes.c_void_p * len(total_ptrs))(*total_ptrs)
+        _lib.call("drk_carry_fold", code, opcode, vals, None, len(total_ptrs), None, None, pair.data_ptr() + 8,
+                  st.index, st.handle)
+        with t.cuda.device(st.index), t.cuda.stream(st.stream):
+            dist.all_gather_into_tensor(gathered, pair, group=group.group)
+        r = group.rank
+        carry_ptr = None
+        if r > 0:
+            g = gathered.data_ptr()
+            vals = (ctypes.c_void_p * r)(*[g + 16 * j + 8 for j in range(r)])
+            has = (ctypes.c_void_p * r)(*[g + 16 * j for j in range(r)])
+            _lib.call("drk_carry_fold", code, opcode, vals, has, r, None, None, carry.data_ptr(), st.index,
+                      st.handle)
+            carry_ptr = carry.data_ptr()
+
+        def host_value():
+            """The carry as the host path computes it (after the scan has completed)."""
+            host = t.empty(2 * group.size, dtype=t.int64, pin_memory=True)
+            _lib.call("drk_readback", host.data_ptr(), gathered.data_ptr(), 16 * group.size, st.index, st.handle)
+            st.synchronize()
+            raw = host.numpy().tobytes()
+            fold = _PYOPS[opname]
+            c = None
+            for j in range(r):
+                if np.frombuffer(raw[16 * j: 16 * j + 8], dtype=np.int64)[0]:
+                    v = np.frombuffer(raw[16 * j + 8: 16 * j + 8 + A.itemsize], dtype=A)[0]
+                    c = v if c is None else fold(c, v)
+            _keep = (pair, gathered, carry)  # noqa: F841 - alive until the scan has run
+            return c
+
+        return carry_ptr, host_value
+
+    return hook

@@ -641,3 +641,50 @@ class TestAsyncTransfers:
             tk.wait()
         for o in outs:
             assert np.array_equal(o, np.arange(1, n + 1, dtype=np.float32))
+
+
+class TestCarryFold:
+    """drk_carry_fold: the reference's driver fold of segment totals (algorithms.py:256-262)
+    on the device, with has-flags as the all-gathered (has, total) pairs of spmd.py carry them."""
+
+    @pytest.mark.parametrize("dtype,op", [(np.float32, "add"), (np.float64, "multiply"), (np.int32, "add"),
+                                          (np.int64, "minimum"), (np.float32, "maximum")])
+    def test_fold_with_has_flags(self, dtype, op):
+        import ctypes
+        import torch
+
+        T = np.dtype(dtype)
+        opcode = {"add": _lib.ADD, "multiply": _lib.MUL, "minimum": _lib.MIN, "maximum": _lib.MAX}[op]
+        A = _lib.acc_dtype(T, opcode)
+        L = np.dtype(np.int64) if (T == np.int32 and op in ("add", "multiply")) else T
+        rng = np.random.default_rng(7)
+        vals = (rng.random(6) * 10 - 3).astype(A) if A.kind == "f" else rng.integers(-50, 50, 6).astype(A)
+        has = np.array([1, 0, 1, 1, 0, 1], dtype=np.int64)
+        buf = np.zeros(12, dtype=np.int64)
+        buf[0::2] = has
+        raw = buf.view(np.uint8).reshape(6, 16)
+        for j in range(6):
+            raw[j, 8:8 + A.itemsize] = np.frombuffer(vals[j:j + 1].tobytes(), dtype=np.uint8)
+        dev = torch.from_numpy(buf.copy()).cuda()
+        out = torch.zeros(2, dtype=torch.int64, device="cuda")
+        fold = {"add": np.add, "multiply": np.multiply, "minimum": np.minimum, "maximum": np.maximum}[op]
+        s = torch.cuda.current_stream()
+        for count, carry_in in ((6, None), (3, 2), (0, None), (0, 5)):
+            ptr = dev.data_ptr()
+            v = (ctypes.c_void_p * 6)(*[ptr + 16 * j + 8 for j in range(6)])
+            h = (ctypes.c_void_p * 6)(*[ptr + 16 * j for j in range(6)])
+            cin = _lib.scalar_buffer(carry_in, A) if carry_in is not None else None
+            _lib.call("drk_carry_fold", _lib.dtype_code(T), opcode, v, h, count,
+                      ctypes.addressof(cin) if cin is not None else None, None, out.data_ptr(), 0, s.cuda_stream)
+            got = np.frombuffer(out.cpu().numpy().tobytes()[:A.itemsize], dtype=A)[0]
+            exp = None if carry_in is None else A.type(carry_in)
+            for j in range(count):
+                if has[j]:
+                    x = A.type(L.type(vals[j]))
+                    exp = x if exp is None else fold(exp, x)
+            if exp is None:  # nothing folded: the fold's identity
+                ident = {"add": -0.0 if A.kind == "f" else 0, "multiply": 1,
+                         "minimum": np.inf if A.kind == "f" else np.iinfo(A).max,
+                         "maximum": -np.inf if A.kind == "f" else np.iinfo(A).min}[op]
+                exp = A.type(ident)
+            assert got == exp and np.signbit(got) == np.signbit(exp), (count, carry_in, got, exp)

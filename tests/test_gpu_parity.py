@@ -84,8 +84,19 @@ def _scan_cases():
     return [c for c in CASES if c["op"] in ("inclusive_scan", "exclusive_scan") and "raises" not in c]
 
 
+@pytest.fixture(params=["single", "device_carry", "host_carry"])
+def schedule(request, monkeypatch):
+    """The scan schedule: one GPU's chained carries, or the multi-GPU two-pass schedule
+    (forced onto the visible GPU) with the carry folded on the device (drk_carry_fold) or
+    on the host."""
+    if request.param != "single":
+        monkeypatch.setattr(A, "_FORCE_MULTI_DEVICE_SCAN", True)
+        monkeypatch.setattr(A, "_FORCE_HOST_CARRY", request.param == "host_carry")
+    return request.param
+
+
 @pytest.mark.parametrize("case", _scan_cases(), ids=[c["id"] for c in _scan_cases()])
-def test_scan(case, rt_pool, gold):
+def test_scan(case, rt_pool, gold, schedule):
     dt = np.dtype(case["dtype"])
     x = O.generate(case["inputs"][0], dt)
     rt = rt_pool(case["p"])
@@ -113,7 +124,7 @@ def test_scan(case, rt_pool, gold):
             np.testing.assert_allclose(got, ref, rtol=REL[case["dtype"]], atol=0)
 
 
-def test_scan_int32_carry_overflow_raises(rt_pool):
+def test_scan_int32_carry_overflow_raises(rt_pool, schedule):
     case = [c for c in CASES if "raises" in c][0]
     x = O.generate(case["inputs"][0], np.int32)
     rt = rt_pool(case["p"])
