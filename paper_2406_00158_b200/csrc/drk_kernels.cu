@@ -142,7 +142,7 @@ static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
 static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
 static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned segments
 static int g_scan_l2_min = 1 << 22;
-static int g_scan_l2_subs = 0;   // sub-tiles per L2 tile (0: 8 = 160 KB for fp32, 7 for int32 sums)
+static int g_scan_l2_subs = 0;   // sub-tiles per L2 tile (0: 8 = 160 KB for 4-byte types)
 static int g_scan_l2_pre = 2;    // sub-tiles scanned prefix-free during the look-back
 static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
 static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
@@ -677,8 +677,8 @@ extern "C" int drk_dot(int dtype, const void* x, const void* y, int64_t n, void*
 
 template <class T, class Op> struct ScanItems {
   // ITEMS * sizeof(T) / 16 odd => conflict-free 16-byte LDS of per-thread runs.
-  static constexpr int value =
-      sizeof(T) == 4 ? (sizeof(typename LocalAcc<T, Op>::type) == 4 ? 20 : 12) : 10;
+  // (int32 sums keep 64-bit running partials; 20 still fits without spills: 64 registers)
+  static constexpr int value = sizeof(T) == 4 ? 20 : 10;
 };
 static constexpr int SCAN_SUB_MAX = 4;
 
@@ -722,9 +722,7 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
 template <class T, class Op>
 static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int IT = ScanItems<T, Op>::value;
-  // int32 sums keep 12-element runs of int64 partials (96 KB at 8 sub-tiles); measured best
-  // at 7 sub-tiles, every other type at 8
-  const int subs = g_scan_l2_subs ? g_scan_l2_subs : (sizeof(T) == 4 && IT == 12 ? 7 : 8);
+  const int subs = g_scan_l2_subs ? g_scan_l2_subs : 8;  // 160 KB tiles (fp32/int32), 8 x 20 KB
   p.pre = g_scan_l2_pre;
   switch (subs) {
     case 7: return launch_scan_l2dyn<T, Op, 7, IT, 3>(p, n, s);
