@@ -408,7 +408,8 @@ def main():
             "data": "synthetic (splitmix64 unit doubles -> fp32, generated on device, reference repro.py)",
             "config": {"workload": "+".join(workloads) + f" fp32, 2^{args.log2n} elements per GPU",
                        "elements_per_gpu": n, "segments_per_gpu": 1, "parallelism": f"dp{world}",
-                       "l2": "inputs 4 GiB per vector >> 126 MB L2 (no flush needed)",
+                       "l2": (f"inputs {n * 4 / 2**30:.3g} GiB per vector = {n * 4 / 126e6:.3g}x the 126 MB L2"
+                              + (" (no flush needed)" if n * 4 > 4 * 126e6 else " (L2-resident: not a DRAM number)")),
                        "frac_of_aggregate_roofline": round(value / (peak * world), 4)},
             "roofline": roofline,
             "workloads": per,
