@@ -135,6 +135,18 @@ int drk_carry_fold(int dtype, int op, const void* const* totals, const void* con
                    const void* carry_in_host, const void* carry_in_dev, void* carry_out_dev, int device,
                    void* stream);
 
+/* drk_scan with flags.  DRK_SCAN_CHAINED: this scan continues a chain of segment scans on
+ * one stream — it is launched as a programmatic dependent of the kernel enqueued just before
+ * (the scan of the previous segment, which writes this scan's carry_dev).  Its tiles reduce
+ * their input while the previous scan drains and wait for it only to read the carry.  The
+ * caller guarantees that the previous kernel on the stream is that scan, that the two
+ * scans' data do not overlap, and that consecutive scans of a chain use different scratch
+ * buffers (alternate two).  Large segments only; otherwise the flag is ignored. */
+#define DRK_SCAN_CHAINED 1
+int drk_scan_ex(int dtype, int op, int exclusive, int flags, const void* in, void* out, int64_t n,
+                const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total_dev,
+                void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream);
+
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
  * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),
  * plus the splitter search of the distributed sample sort; the runtime moves the runs

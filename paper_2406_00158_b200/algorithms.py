@@ -323,10 +323,13 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list
         prev_carry = None
         for j, (k, _, launch, in_ptr, tgt) in enumerate(work):
             first_carry = _to_acc(carry, A) if (j == 0 and carry is not None) else None
+            # segment j's carry is written by segment j-1's scan, enqueued just before: chain
+            # them (programmatic dependent launch) so j's tiles reduce while j-1 drains
             run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a,
                      carry_value=first_carry,
                      carry_dev=st.result_dev_ptr(prev_carry) if prev_carry is not None else None,
-                     seg_total_slot=2 * j, carry_out_slot=2 * j + 1)
+                     seg_total_slot=2 * j, carry_out_slot=2 * j + 1,
+                     chained=prev_carry is not None and _CHAIN_SCANS, scratch_index=j % 2)
             prev_carry = 2 * j + 1
         raw = st.fetch_results(2 * len(work))
         for j, (k, *_rest) in enumerate(work):
@@ -374,6 +377,7 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list
 # (_FORCE_MULTI_DEVICE_SCAN), or fold its carries on the host (_FORCE_HOST_CARRY).
 _FORCE_MULTI_DEVICE_SCAN = False
 _FORCE_HOST_CARRY = False
+_CHAIN_SCANS = True  # programmatic dependent launches for consecutive segment scans on one GPU
 
 
 def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, init, init_a, carry, launches,

@@ -146,6 +146,7 @@ static int g_scan_l2_subs = 0;   // sub-tiles per L2 tile (0: 8 = 160 KB for 4-b
 static int g_scan_l2_pre = 2;    // sub-tiles scanned prefix-free during the look-back
 static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
 static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
+static thread_local int g_chain_launch = 0;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
 static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
                                  // measured slower than one 120 KB tile per CTA
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
@@ -714,7 +715,29 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
   } else {
     auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, false, RING>;
     DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
+    // With more than two waves of tiles, every CTA lets a chained successor launch as soon as
+    // it starts (a no-op unless the next kernel is a DRK_SCAN_CHAINED scan): all of this grid
+    // has started only after most of it has finished, i.e. after its own wait for the scan
+    // before it, whose scratch the successor reuses.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    p2.early_trigger = nt > 2 * (int64_t)sm_count(dev) * occupancy(k, BLOCK, smem);
+    if (g_chain_launch) {
+      // programmatic dependent of the previous scan of the chain (see carry_dev_read)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)nt);
+      cfg.blockDim = dim3(BLOCK);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      DRK_CHECK(cudaLaunchKernelEx(&cfg, k, p2));
+    } else {
+      k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
+    }
   }
   return 0;
 }
@@ -841,6 +864,20 @@ extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* 
     return scan_op<T>(op, exclusive, (const T*)in, (T*)out, n, init_host, carry_host, carry_dev, seg_total_dev,
                       carry_out_dev, scratch, scratch_bytes, device, stream);
   });
+}
+
+extern "C" int drk_scan_ex(int dtype, int op, int exclusive, int flags, const void* in, void* out, int64_t n,
+                           const void* init_host, const void* carry_host, const void* carry_dev,
+                           void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,
+                           void* stream) {
+  if (flags & ~DRK_SCAN_CHAINED) return set_error(DRK_E_ARG, "drk_scan_ex: unknown flags");
+  if ((flags & DRK_SCAN_CHAINED) && !carry_dev)
+    return set_error(DRK_E_ARG, "drk_scan_ex: a chained scan takes its carry from the previous scan (carry_dev)");
+  g_chain_launch = (flags & DRK_SCAN_CHAINED) != 0;
+  const int rc = drk_scan(dtype, op, exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total_dev,
+                          carry_out_dev, scratch, scratch_bytes, device, stream);
+  g_chain_launch = 0;
+  return rc;
 }
 
 // ---------------------------------------------------------------------------------------

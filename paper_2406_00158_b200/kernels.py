@@ -60,7 +60,8 @@ def launch_kernel(name, launch_ctx, n, *args):
     s.record(launch_ctx.state.stream)
     _lib.call(name, *args, launch_ctx.device, launch_ctx.stream)
     e.record(launch_ctx.state.stream)
-    _PROFILE.setdefault(name, []).append((s, e, n))
+    key = name[:-3] if name.endswith("_ex") else name  # drk_scan_ex is reported as drk_scan
+    _PROFILE.setdefault(key, []).append((s, e, n))
 
 
 def launch_jit(mod, kernel, grid, block, smem, buf, nbytes, lctx, n):
@@ -274,18 +275,23 @@ def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
 
 
 def run_scan(dtype, opcode, exclusive, in_ptr, out_ptr, n, lctx: Launch, *, init=None, carry_value=None,
-             carry_dev=None, seg_total_slot=None, carry_out_slot=None):
-    """One drk_scan over a plain device buffer (the caller materialises views first)."""
+             carry_dev=None, seg_total_slot=None, carry_out_slot=None, chained=False, scratch_index=0):
+    """One drk_scan over a plain device buffer (the caller materialises views first).
+
+    chained: this scan continues a chain of segment scans on the stream (its carry_dev is
+    written by the scan enqueued just before; drk_scan_ex DRK_SCAN_CHAINED), and
+    scratch_index alternates the scratch buffer between consecutive scans of the chain."""
     T = np.dtype(dtype)
     code = _lib.dtype_code(T)
     A = _lib.acc_dtype(T, opcode)
     st = lctx.state
     nbytes = int(_lib.load().drk_scan_scratch_bytes(code, opcode, n))
-    scratch = st.scan_scratch(nbytes)
+    scratch = st.scan_scratch(nbytes, scratch_index)
     init_buf = _keep(lctx, _scalar_arg(init, A)) if init is not None else None
     carry_buf = _keep(lctx, _scalar_arg(carry_value, A)) if carry_value is not None else None
     launch_kernel(
-        "drk_scan", lctx, n, code, opcode, 1 if exclusive else 0, in_ptr, out_ptr, n,
+        "drk_scan_ex", lctx, n, code, opcode, 1 if exclusive else 0, _lib.SCAN_CHAINED if chained else 0,
+        in_ptr, out_ptr, n,
         ctypes.addressof(init_buf) if init_buf is not None else None,
         ctypes.addressof(carry_buf) if carry_buf is not None else None,
         carry_dev,

@@ -117,13 +117,19 @@ class DeviceState:
             self.reduce_scratch = None
 
     # -- scratch ---------------------------------------------------------
-    def scan_scratch(self, nbytes: int):
+    def scan_scratch(self, nbytes: int, which: int = 0):
+        """Scan scratch buffer `which` (0 or 1: consecutive scans of a chained launch
+        alternate, kernels.run_scan)."""
         t = torch()
-        if self._scan_scratch is None or self._scan_scratch.numel() < nbytes:
+        if self._scan_scratch is None:
+            self._scan_scratch = [None, None]
+        buf = self._scan_scratch[which]
+        if buf is None or buf.numel() < nbytes:
             with t.cuda.stream(self.stream):
                 # zero once: tile descriptors are epoch-tagged, the ticket counter self-resets
-                self._scan_scratch = t.zeros(int(nbytes * 1.25) + 4096, dtype=t.uint8, device=self.device)
-        return self._scan_scratch
+                buf = t.zeros(int(nbytes * 1.25) + 4096, dtype=t.uint8, device=self.device)
+            self._scan_scratch[which] = buf
+        return buf
 
     def ensure_results(self, slots: int):
         if slots <= self._result_slots:
