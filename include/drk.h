@@ -147,6 +147,19 @@ int drk_scan_ex(int dtype, int op, int exclusive, int flags, const void* in, voi
                 const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total_dev,
                 void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream);
 
+/* Batched segment scan: the nseg (<= DRK_SCAN_SEGS) segments of a vector that live on one GPU
+ * — ins[k] -> outs[k], ns[k] >= 1 elements, 16-byte aligned — scanned in one launch as one
+ * sequence (algorithms.py:234-308 with the carries between them folded by the look-back),
+ * starting from carry_host or carry_dev.  seg_totals_dev (nullable) receives each segment's
+ * own total in 8-byte slots (accumulator type), carry_out_dev (nullable) the carry after the
+ * last segment.  Scratch: drk_scan_batch_scratch_bytes (zeroed once, reusable). */
+#define DRK_SCAN_SEGS 16
+size_t drk_scan_batch_scratch_bytes(int dtype, int op, int nseg, const int64_t* ns);
+int drk_scan_batch(int dtype, int op, int exclusive, int nseg, const void* const* ins, void* const* outs,
+                   const int64_t* ns, const void* init_host, const void* carry_host, const void* carry_dev,
+                   void* seg_totals_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,
+                   void* stream);
+
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
  * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),
  * plus the splitter search of the distributed sample sort; the runtime moves the runs

@@ -317,8 +317,13 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list
         init_a = _to_acc(init, A)
 
     if len(devices) == 1 and not _FORCE_MULTI_DEVICE_SCAN and carry_hook is None:
-        # single device: chain the carry on the device, one pass per segment
         st = work[0][1]
+        m = len(work)
+        if (_BATCH_SCANS and 1 < m <= _lib.SCAN_SEGS and sum(w[4].length for w in work) >= _BATCH_MIN
+                and all(w[3] % 16 == 0 and w[4].ptr() % 16 == 0 for w in work)):
+            # single device, several segments: one batched launch scans them as one sequence
+            return _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry)
+        # single device: chain the carry on the device, one pass per segment
         st.ensure_results(2 * len(work) + 2)
         prev_carry = None
         for j, (k, _, launch, in_ptr, tgt) in enumerate(work):
@@ -378,6 +383,36 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list
 _FORCE_MULTI_DEVICE_SCAN = False
 _FORCE_HOST_CARRY = False
 _CHAIN_SCANS = True  # programmatic dependent launches for consecutive segment scans on one GPU
+_BATCH_SCANS = True  # one drk_scan_batch launch for the segments a GPU holds (up to SCAN_SEGS)
+_BATCH_MIN = 1 << 20  # below this many elements the chained single-pass scans are cheaper
+
+
+def _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry):
+    """The segments on one GPU scanned by one drk_scan_batch launch: the L2 scan runs over
+    their concatenation, so the look-back carries the prefix from segment to segment
+    (algorithms.py:256-262 without a pass per segment), and the per-segment totals — the
+    reference's partials — are folded from the tile aggregates afterwards."""
+    code = _lib.dtype_code(T)
+    m = len(work)
+    ins = (ctypes.c_void_p * m)(*[w[3] for w in work])
+    outs = (ctypes.c_void_p * m)(*[w[4].ptr() for w in work])
+    ns = (ctypes.c_int64 * m)(*[w[4].length for w in work])
+    nbytes = int(_lib.load().drk_scan_batch_scratch_bytes(code, opcode, m, ns))
+    scratch = st.scan_scratch(nbytes, 0)
+    st.ensure_results(m)
+    launch = work[0][2]
+    init_buf = _lib.scalar_buffer(init_a, A) if init_a is not None else None
+    carry_buf = _lib.scalar_buffer(_to_acc(carry, A), A) if carry is not None else None
+    kernels.launch_kernel("drk_scan_batch", launch, sum(ns), code, opcode, 1 if exclusive else 0, m, ins, outs, ns,
+                          ctypes.addressof(init_buf) if init_buf is not None else None,
+                          ctypes.addressof(carry_buf) if carry_buf is not None else None, None,
+                          st.result_dev_ptr(0), None, scratch.data_ptr(), scratch.numel())
+    raw = st.fetch_results(m)
+    for j, (k, *_rest) in enumerate(work):
+        total = np.frombuffer(raw[8 * j: 8 * j + A.itemsize].tobytes(), dtype=A)[0]
+        partials[k] = total.astype(L).item()
+    _check_carry_range(op, partials, live, exclusive, init, T, carry)
+    return partials
 
 
 def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, init, init_a, carry, launches,

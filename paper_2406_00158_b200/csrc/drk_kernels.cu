@@ -866,6 +866,140 @@ extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* 
   });
 }
 
+// ---------------------------------------------------------------------------------------
+// batched segments: one L2-scan launch over the concatenation of up to DRK_SCAN_SEGS buffers
+// on one GPU (the segments of a vector that share a device), so the look-back carries the
+// prefix from segment to segment and there is one ramp-up and one tail instead of one per
+// segment.  Per-segment totals (the reference's partials, algorithms.py:234-274) are folded
+// afterwards from the per-tile aggregates, one warp per segment, in tile order.
+
+template <class T, class Op>
+__global__ void __launch_bounds__(256) seg_totals_kernel(const u64* aggs,
+                                                         const ScanParams<typename WideAcc<T, Op>::type, const T*> p,
+                                                         char* out) {
+  typedef typename WideAcc<T, Op>::type A;
+  __shared__ Opt<A> s_warp[8];
+  const int k = blockIdx.x;
+  const u32 lo = p.seg_first[k], hi = p.seg_first[k + 1];
+  const u32 per = (hi - lo + 255) / 256;
+  const u32 a = lo + threadIdx.x * per;
+  Opt<A> acc;
+  acc.has = 0;
+  acc.v = A();
+  for (u32 t0 = a; t0 < a + per && t0 < hi; t0 += 8) {
+    u64 w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = (t0 + u < a + per && t0 + u < hi) ? __ldcg(aggs + t0 + u) : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (t0 + u < a + per && t0 + u < hi) {
+        Opt<A> v;
+        v.has = 1;
+        v.v = from_bits<A>(w[u]);
+        acc = opt_combine<Op>(acc, v);
+      }
+    }
+  }
+  const Opt<A> tot = block_reduce<Op, A, 256>(acc, s_warp);  // thread order = tile order
+  if (threadIdx.x == 0) *(A*)(out + 8 * (size_t)k) = tot.v;
+}
+
+template <class T, class Op>
+static int launch_scan_batch(int exclusive, int nseg, const void* const* ins, void* const* outs, const int64_t* ns,
+                             const void* init_host, const void* carry_host, const void* carry_dev, void* seg_totals,
+                             void* carry_out, void* scratch, size_t scratch_bytes, int device, void* stream) {
+  typedef typename WideAcc<T, Op>::type A;
+  constexpr int IT = ScanItems<T, Op>::value;
+  constexpr int SUBS = 8;
+  constexpr int TILE = BLOCK * IT * SUBS;
+  const char* what = "drk_scan_batch";
+  if (nseg < 1 || nseg > DRK_SCAN_SEGS) return set_error(DRK_E_ARG, "drk_scan_batch: nseg out of range");
+  if (exclusive && !init_host) return set_error(DRK_E_ARG, "drk_scan_batch: exclusive scan needs init");
+  if (carry_host && carry_dev) return set_error(DRK_E_ARG, "drk_scan_batch: give at most one carry");
+  ScanParams<A, const T*> p;
+  memset(&p, 0, sizeof(p));
+  u64 nt = 0;
+  for (int k = 0; k < nseg; ++k) {
+    if (ns[k] < 1 || !ins[k] || !outs[k]) return set_error(DRK_E_ARG, "drk_scan_batch: empty or null segment");
+    if (!aligned16(ins[k]) || !aligned16(outs[k]))
+      return set_error(DRK_E_ARG, "drk_scan_batch: segments must be 16-byte aligned");
+    p.seg_first[k] = (u32)nt;
+    p.seg_in[k] = ins[k];
+    p.seg_out[k] = outs[k];
+    p.seg_n[k] = ns[k];
+    nt += (u64)((ns[k] + TILE - 1) / TILE);
+  }
+  p.seg_first[nseg] = (u32)nt;
+  if (nt > 0x7fffffffull) return set_error(DRK_E_ARG, "drk_scan_batch: too many tiles");
+  const size_t need = 128 + nt * 16 + nt * 8;
+  if (!scratch || scratch_bytes < need)
+    return set_error(DRK_E_SCRATCH, "drk_scan_batch: scratch too small (need " + std::to_string(need) + ")");
+  if (int rc = prologue(device, what)) return rc;
+  char* b = (char*)scratch;
+  p.nseg = nseg;
+  p.ntiles = (u32)nt;
+  p.exclusive = exclusive;
+  p.has_init = init_host != nullptr;
+  if (init_host) memcpy(&p.init, init_host, sizeof(A));
+  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
+  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
+  p.carry_ptr = (const A*)carry_dev;
+  p.carry_out = (A*)carry_out;
+  p.counter = (u32*)b;
+  p.desc = (u64*)(b + 128);
+  p.aggs = (u64*)(b + 128 + nt * 16);
+  p.epoch = next_epoch(scratch);
+  p.bulk_ok = 1;
+  p.pre = g_scan_l2_pre;
+  p.debug = g_scan_debug;
+  const int smem = 3 * BLOCK * IT * (int)sizeof(T);
+  auto k = scan_l2_kernel<T, Op, BLOCK, IT, SUBS, false, 3>;
+  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k<<<(unsigned)nt, BLOCK, smem, (cudaStream_t)stream>>>(p);
+  if (seg_totals) seg_totals_kernel<T, Op><<<nseg, 256, 0, (cudaStream_t)stream>>>(p.aggs, p, (char*)seg_totals);
+  return epilogue(what);
+}
+
+extern "C" size_t drk_scan_batch_scratch_bytes(int dtype, int op, int nseg, const int64_t* ns) {
+  (void)op;
+  const int64_t tile = (int64_t)BLOCK * 8 * ((dtype == DRK_F64 || dtype == DRK_I64) ? 10 : 20);
+  size_t nt = 0;
+  for (int k = 0; k < nseg; ++k) nt += (size_t)((ns[k] + tile - 1) / tile);
+  return 128 + nt * 24;
+}
+
+template <class T>
+static int scan_batch_op(int op, int exclusive, int nseg, const void* const* ins, void* const* outs, const int64_t* ns,
+                         const void* init_host, const void* carry_host, const void* carry_dev, void* seg_totals,
+                         void* carry_out, void* scratch, size_t sb, int device, void* stream) {
+  switch (op) {
+    case DRK_ADD:
+      return launch_scan_batch<T, OpAdd>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
+                                         carry_out, scratch, sb, device, stream);
+    case DRK_MUL:
+      return launch_scan_batch<T, OpMul>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
+                                         carry_out, scratch, sb, device, stream);
+    case DRK_MIN:
+      return launch_scan_batch<T, OpMin>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
+                                         carry_out, scratch, sb, device, stream);
+    case DRK_MAX:
+      return launch_scan_batch<T, OpMax>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
+                                         carry_out, scratch, sb, device, stream);
+  }
+  return set_error(DRK_E_ARG, "drk_scan_batch: unknown op");
+}
+
+extern "C" int drk_scan_batch(int dtype, int op, int exclusive, int nseg, const void* const* ins, void* const* outs,
+                              const int64_t* ns, const void* init_host, const void* carry_host, const void* carry_dev,
+                              void* seg_totals_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
+                              int device, void* stream) {
+  if (!ins || !outs || !ns) return set_error(DRK_E_ARG, "drk_scan_batch: null segment arrays");
+  DRK_DISPATCH(dtype, "drk_scan_batch", T, {
+    return scan_batch_op<T>(op, exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals_dev,
+                            carry_out_dev, scratch, scratch_bytes, device, stream);
+  });
+}
+
 extern "C" int drk_scan_ex(int dtype, int op, int exclusive, int flags, const void* in, void* out, int64_t n,
                            const void* init_host, const void* carry_host, const void* carry_dev,
                            void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,

@@ -84,12 +84,15 @@ def _scan_cases():
     return [c for c in CASES if c["op"] in ("inclusive_scan", "exclusive_scan") and "raises" not in c]
 
 
-@pytest.fixture(params=["single", "device_carry", "host_carry"])
+@pytest.fixture(params=["single", "batched", "device_carry", "host_carry"])
 def schedule(request, monkeypatch):
-    """The scan schedule: one GPU's chained carries, or the multi-GPU two-pass schedule
-    (forced onto the visible GPU) with the carry folded on the device (drk_carry_fold) or
-    on the host."""
-    if request.param != "single":
+    """The scan schedule: one GPU's chained carries ("single": golden sizes are below the
+    batching threshold), one batched launch over the GPU's segments (drk_scan_batch), or the
+    multi-GPU two-pass schedule (forced onto the visible GPU) with the carry folded on the
+    device (drk_carry_fold) or on the host."""
+    if request.param == "batched":
+        monkeypatch.setattr(A, "_BATCH_MIN", 1)
+    elif request.param != "single":
         monkeypatch.setattr(A, "_FORCE_MULTI_DEVICE_SCAN", True)
         monkeypatch.setattr(A, "_FORCE_HOST_CARRY", request.param == "host_carry")
     return request.param
