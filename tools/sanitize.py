@@ -5,8 +5,8 @@ family once on small and ragged sizes, through the public API, checked against n
     compute-sanitizer --tool racecheck python tools/sanitize.py --small
 
 Covers map (copy, fill, iota, triad, Black-Scholes, NVRTC maps), reduce (dot, sum/min/max,
-NVRTC reduce), scan (single-pass tiles; the L2 two-touch kernel at n >= 2^22 unless
---small), sort (both strategies: CUB, drk_gather, drk_sort_bounds) and the readback kernel.
+NVRTC reduce), scan (single-pass tiles, the L2 two-touch kernel, chained and batched over
+segments), sort (both strategies: CUB, drk_gather, drk_sort_bounds) and the readback kernel.
 """
 import os
 import sys
@@ -48,15 +48,18 @@ for n in sizes:
     assert A.reduce(vi, 0) == int(xi.astype(np.int64).sum())
     assert A.reduce(vi, 10**9, A.minimum) == int(xi.min())
     assert A.reduce(views.transform(vi, lambda v: v % 7), 0) == int((xi % 7).astype(np.int64).sum())
-    # scan kernels (aligned, unaligned view, exclusive)
-    o = sr.DistributedVector(rt, n, dtype=np.int32)
-    A.inclusive_scan(vi, o)
-    assert np.array_equal(o.to_numpy(), np.cumsum(xi.astype(np.int64)).astype(np.int32))
-    if n > 3:
-        o2 = sr.DistributedVector(rt, n - 3, dtype=np.int32)
-        A.exclusive_scan(views.drop(vi, 3), o2, 5)
-        exp = 5 + np.concatenate([[0], np.cumsum(xi[3:].astype(np.int64))[:-1]])
-        assert np.array_equal(o2.to_numpy(), exp.astype(np.int32))
+    # scan kernels (aligned, unaligned view, exclusive), chained and batched over the segments
+    for batch_min in (1 << 20, 1):
+        A._BATCH_MIN = batch_min
+        o = sr.DistributedVector(rt, n, dtype=np.int32)
+        A.inclusive_scan(vi, o)
+        assert np.array_equal(o.to_numpy(), np.cumsum(xi.astype(np.int64)).astype(np.int32))
+        if n > 3:
+            o2 = sr.DistributedVector(rt, n - 3, dtype=np.int32)
+            A.exclusive_scan(views.drop(vi, 3), o2, 5)
+            exp = 5 + np.concatenate([[0], np.cumsum(xi[3:].astype(np.int64))[:-1]])
+            assert np.array_equal(o2.to_numpy(), exp.astype(np.int32))
+    A._BATCH_MIN = 1 << 20
     # sort (gather + sample strategies, keyed)
     for strategy in ("gather", "sample"):
         s = sr.DistributedVector.from_numpy(rt, xi)
