@@ -160,6 +160,16 @@ int drk_scan_batch(int dtype, int op, int exclusive, int nseg, const void* const
                    void* seg_totals_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,
                    void* stream);
 
+/* Batched reductions (algorithms.py:153-162 `_reduce_task` for every segment a GPU holds, one
+ * launch): results receives one 8-byte slot per segment (accumulator type, drk_acc_dtype),
+ * scratch is nseg x drk_reduce_scratch_bytes().  nseg <= DRK_RED_SEGS. */
+#define DRK_RED_SEGS 16
+int drk_reduce_batch(int dtype, int op, int nseg, const void* const* xs, const int64_t* ns, void* results,
+                     void* scratch, int device, void* stream);
+/* bench.py:87-90 dot_product over every segment pair a GPU holds, one launch */
+int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                  void* results, void* scratch, int device, void* stream);
+
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
  * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),
  * plus the splitter search of the distributed sample sort; the runtime moves the runs

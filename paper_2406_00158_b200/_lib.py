@@ -78,6 +78,9 @@ SIGNATURES = {
     "drk_dot": (_int, [_int, _vp, _vp, _i64, _vp, _vp, _int, _vp]),
     "drk_scan_scratch_bytes": (_sz, [_int, _int, _i64]),
     "drk_scan": (_int, [_int, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
+    "drk_reduce_batch": (_int, [_int, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp, _int, _vp]),
+    "drk_dot_batch": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp,
+                             _int, _vp]),
     "drk_scan_batch_scratch_bytes": (_sz, [_int, _int, _int, ctypes.POINTER(_i64)]),
     "drk_scan_batch": (_int, [_int, _int, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                               _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
@@ -172,6 +175,7 @@ def launch_count() -> int:
 CARRY_MAX = 64  # drk.h DRK_CARRY_MAX: predecessors one drk_carry_fold call folds
 SCAN_CHAINED = 1  # drk.h DRK_SCAN_CHAINED
 SCAN_SEGS = 16  # drk.h DRK_SCAN_SEGS
+RED_SEGS = 16  # drk.h DRK_RED_SEGS
 
 # sort / gather / bounds also take unsigned keys (drk.h DRK_U32 / DRK_U64)
 SORT_DTYPE_CODE = {**DTYPE_CODE, np.dtype(np.uint32): 4, np.dtype(np.uint64): 5}

@@ -204,7 +204,10 @@ def _segment_partials(rt, pieces, op):
     slots = {}
     order = []
     launches = {}
-    for lw in lowered:
+    batched = _batch_reduce(rt, lowered, opcode) if opcode is not None else None
+    if batched is not None:
+        order, launches, slots = batched
+    for lw in lowered if batched is None else ():
         st = rt.state_of(lw.rank if lw.rank is not None else 0)
         launch = launches.setdefault(id(st), Launch(st))
         slot = slots.get(id(st), 0)
@@ -223,6 +226,40 @@ def _segment_partials(rt, pieces, op):
             a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + vdt.itemsize].tobytes(), dtype=vdt)[0]
             out.append(a.item())
     return out
+
+
+def _batch_reduce(rt, lowered, opcode):
+    """Several segments on one GPU, each a catalogue reduction (a plain device array, or the
+    product of two for dot): one drk_reduce_batch / drk_dot_batch launch instead of one
+    launch per segment.  Returns (order, launches, slots) like the per-segment loop, or None
+    when the pieces do not qualify."""
+    from .runtime import await_pending
+
+    m = len(lowered)
+    if not 1 < m <= _lib.RED_SEGS:
+        return None
+    states = {id(rt.state_of(lw.rank if lw.rank is not None else 0)) for lw in lowered}
+    if len(states) != 1:
+        return None
+    st = rt.state_of(lowered[0].rank if lowered[0].rank is not None else 0)
+    plans = [kernels.catalogue_reduce(lw.value, lw.leaves, opcode, st.index) for lw in lowered]
+    if any(p is None for p in plans) or len({(p[0], p[1]) for p in plans}) != 1:
+        return None
+    kind, code = plans[0][0], plans[0][1]
+    await_pending(st, [lf.handle for lw in lowered for lf in lw.leaves if lf.handle is not None])
+    launch = Launch(st)
+    ns = (ctypes.c_int64 * m)(*[lw.length for lw in lowered])
+    xs = (ctypes.c_void_p * m)(*[p[2] for p in plans])
+    scratch = st.reduce_batch_scratch(m)
+    if kind == "reduce":
+        kernels.launch_kernel("drk_reduce_batch", launch, sum(ns), code, opcode, m, xs, ns,
+                              st.host_result_dev_ptr(0), scratch.data_ptr())
+    else:
+        ys = (ctypes.c_void_p * m)(*[p[3] for p in plans])
+        kernels.launch_kernel("drk_dot_batch", launch, sum(ns), code, m, xs, ys, ns,
+                              st.host_result_dev_ptr(0), scratch.data_ptr())
+    order = [(st, j, lw.value.dtype) for j, lw in enumerate(lowered)]
+    return order, {id(st): launch}, {id(st): m}
 
 
 # ----------------------------------------------------------------------------------------

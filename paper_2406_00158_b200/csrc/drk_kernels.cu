@@ -663,6 +663,94 @@ extern "C" int drk_reduce(int dtype, int op, const void* x, int64_t n, void* res
   DRK_DISPATCH(dtype, "drk_reduce", T, { return reduce_op<T>(op, (const T*)x, n, result_dev, scratch, device, stream); });
 }
 
+// Batched reductions: the segments of a vector that share a GPU reduced by one launch; the
+// one wave of CTAs is split between the segments in proportion to their lengths, and each
+// segment folds its own CTA partials (same determinism as drk_reduce).  `results` gets one
+// 8-byte slot per segment, `scratch` nseg x drk_reduce_scratch_bytes().
+template <class LD, class Op>
+static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const int64_t* ns, const bool* vec_ok,
+                               void* results, void* scratch, int device, void* stream, const char* what) {
+  typedef typename WideAcc<typename LD::V, Op>::type A;
+  if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, std::string(what) + ": nseg out of range");
+  if (!results || !scratch) return set_error(DRK_E_ARG, std::string(what) + ": null results/scratch");
+  int64_t total = 0;
+  for (int k = 0; k < nseg; ++k) {
+    if (ns[k] < 1) return set_error(DRK_E_ARG, std::string(what) + ": empty segment");
+    total += ns[k];
+  }
+  if (int rc = prologue(device, what)) return rc;
+  auto kern = reduce_batch_kernel<LD, Op, BLOCK, RED_U>;
+  const int64_t cap = (int64_t)sm_count(device) * occupancy(kern, BLOCK, 0) * (g_reduce_waves > 0 ? g_reduce_waves : 1);
+  ReduceBatch<LD, A> b;
+  memset(&b, 0, sizeof(b));
+  b.nseg = nseg;
+  u32 first = 0;
+  const size_t sbytes = 128 + (size_t)MAX_RED_GRID * (8 + 4);
+  for (int k = 0; k < nseg; ++k) {
+    const int64_t work = vec_ok[k] ? (ns[k] / LD::E) + 1 : ns[k];
+    int64_t g = (work + (int64_t)BLOCK * RED_U - 1) / ((int64_t)BLOCK * RED_U);
+    const int64_t share = (cap * ns[k] + total - 1) / total;
+    if (g > share) g = share;
+    if (g > MAX_RED_GRID) g = MAX_RED_GRID;
+    if (g < 1) g = 1;
+    b.cta_first[k] = first;
+    first += (u32)g;
+    b.p[k] = ps[k];
+    b.n[k] = ns[k];
+    b.vec_ok[k] = vec_ok[k] ? 1 : 0;
+    b.s[k] = carve_reduce((char*)scratch + (size_t)k * sbytes);
+    b.result[k] = (A*)((char*)results + 8 * (size_t)k);
+  }
+  b.cta_first[nseg] = first;
+  kern<<<first, BLOCK, 0, (cudaStream_t)stream>>>(b);
+  return epilogue(what);
+}
+
+template <class T>
+static int reduce_batch_op(int op, int nseg, const void* const* xs, const int64_t* ns, void* results, void* scratch,
+                           int device, void* stream) {
+  typename IdentLoad<T>::Params ps[DRK_RED_SEGS];
+  bool v[DRK_RED_SEGS];
+  if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_reduce_batch: nseg out of range");
+  for (int k = 0; k < nseg; ++k) {
+    if (!xs[k]) return set_error(DRK_E_ARG, "drk_reduce_batch: null segment");
+    ps[k].x = (const T*)xs[k];
+    v[k] = aligned16(xs[k]);
+  }
+  const char* w = "drk_reduce_batch";
+  switch (op) {
+    case DRK_ADD: return launch_reduce_batch<IdentLoad<T>, OpAdd>(nseg, ps, ns, v, results, scratch, device, stream, w);
+    case DRK_MUL: return launch_reduce_batch<IdentLoad<T>, OpMul>(nseg, ps, ns, v, results, scratch, device, stream, w);
+    case DRK_MIN: return launch_reduce_batch<IdentLoad<T>, OpMin>(nseg, ps, ns, v, results, scratch, device, stream, w);
+    case DRK_MAX: return launch_reduce_batch<IdentLoad<T>, OpMax>(nseg, ps, ns, v, results, scratch, device, stream, w);
+  }
+  return set_error(DRK_E_ARG, "drk_reduce_batch: unknown op");
+}
+
+extern "C" int drk_reduce_batch(int dtype, int op, int nseg, const void* const* xs, const int64_t* ns, void* results,
+                                void* scratch, int device, void* stream) {
+  if (!xs || !ns) return set_error(DRK_E_ARG, "drk_reduce_batch: null segment arrays");
+  DRK_DISPATCH(dtype, "drk_reduce_batch", T,
+               { return reduce_batch_op<T>(op, nseg, xs, ns, results, scratch, device, stream); });
+}
+
+extern "C" int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                             void* results, void* scratch, int device, void* stream) {
+  if (!xs || !ys || !ns) return set_error(DRK_E_ARG, "drk_dot_batch: null segment arrays");
+  if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_dot_batch: nseg out of range");
+  DRK_DISPATCH(dtype, "drk_dot_batch", T, {
+    typename ProdLoad<T>::Params ps[DRK_RED_SEGS];
+    bool v[DRK_RED_SEGS];
+    for (int k = 0; k < nseg; ++k) {
+      if (!xs[k] || !ys[k]) return set_error(DRK_E_ARG, "drk_dot_batch: null segment");
+      ps[k] = typename ProdLoad<T>::Params{(const T*)xs[k], (const T*)ys[k]};
+      v[k] = aligned16(xs[k]) && aligned16(ys[k]);
+    }
+    return launch_reduce_batch<ProdLoad<T>, OpAdd>(nseg, ps, ns, v, results, scratch, device, stream,
+                                                  "drk_dot_batch");
+  });
+}
+
 extern "C" int drk_dot(int dtype, const void* x, const void* y, int64_t n, void* result_dev, void* scratch,
                        int device, void* stream) {
   if (need(x, "drk_dot", "x") || need(y, "drk_dot", "y")) return DRK_E_ARG;

@@ -246,6 +246,28 @@ class _TensorLeaf(Leaf):
 # reduce
 
 
+def catalogue_reduce(node, leaves, opcode, device):
+    """The batched form of run_reduce's catalogue match for a segment whose leaves are plain
+    device arrays on `device`: ("reduce", dtype code, ptr) or ("dot", code, ptr_x, ptr_y),
+    else None."""
+    T = node.dtype
+    if opcode is None or T not in _lib.DTYPE_CODE:
+        return None
+    code = _lib.DTYPE_CODE[T]
+
+    def arr(k):
+        lf = leaves[k]
+        return lf.kind == "array" and lf.handle is not None and lf.device == device
+
+    if node.op == "leaf" and arr(node.value):
+        return ("reduce", code, leaves[node.value].ptr())
+    if (opcode == _lib.ADD and node.op == "multiply" and _uniform(node, T)
+            and all(_is_leaf(a, leaves) and arr(a.value) for a in node.args)):
+        a, b = node.args
+        return ("dot", code, leaves[a.value].ptr(), leaves[b.value].ptr())
+    return None
+
+
 def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
     """Reduce `node` over n elements into host result slot `slot` of launch.state (value in
     drk_acc_dtype(node.dtype, op) for catalogue ops; read with fetch_host_results)."""

@@ -131,6 +131,18 @@ class DeviceState:
             self._scan_scratch[which] = buf
         return buf
 
+    def reduce_batch_scratch(self, nseg: int):
+        """Scratch of a batched reduction over nseg segments (drk_reduce_batch): nseg reduce
+        scratch blocks, zeroed once (their tickets reset themselves)."""
+        t = torch()
+        per = int(_lib.load().drk_reduce_scratch_bytes())
+        buf = getattr(self, "_reduce_batch_scratch", None)
+        if buf is None or buf.numel() < nseg * per:
+            with t.cuda.stream(self.stream):
+                buf = t.zeros(max(nseg, 4) * per, dtype=t.uint8, device=self.device)
+            self._reduce_batch_scratch = buf
+        return buf
+
     def ensure_results(self, slots: int):
         if slots <= self._result_slots:
             return
