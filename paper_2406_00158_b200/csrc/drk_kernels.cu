@@ -769,7 +769,6 @@ template <class T, class Op> struct ScanItems {
   // (int32 sums keep 64-bit running partials; 20 still fits without spills: 64 registers)
   static constexpr int value = sizeof(T) == 4 ? 20 : 10;
 };
-static constexpr int SCAN_SUB_MAX = 4;
 
 template <class T, class Op> static size_t scan_scratch(int64_t n) {
   // sized for the smallest tile (SUB = 1) so any g_scan_sub fits
