@@ -688,3 +688,63 @@ class TestCarryFold:
                          "maximum": -np.inf if A.kind == "f" else np.iinfo(A).min}[op]
                 exp = A.type(ident)
             assert got == exp and np.signbit(got) == np.signbit(exp), (count, carry_in, got, exp)
+
+
+class TestBatchedSegments:
+    """One launch over all the segments a GPU holds (drk_scan_batch, drk_reduce_batch,
+    drk_dot_batch) against numpy, including the shapes that must fall back to per-segment
+    launches (more than 16 segments, unaligned views, tiny totals)."""
+
+    @pytest.mark.parametrize("p", [2, 5, 16, 17])
+    @pytest.mark.parametrize("dtype", [np.int32, np.float64])
+    def test_scan_and_reduce(self, rt_pool, monkeypatch, p, dtype):
+        from paper_2406_00158_b200 import algorithms as A
+
+        monkeypatch.setattr(A, "_BATCH_MIN", 1)
+        n = 300_007
+        x = O.mod_ints(4, 0, n, 2001, -1000).astype(dtype)
+        rt = rt_pool(p)
+        v = sr.DistributedVector.from_numpy(rt, x)
+        out = sr.DistributedVector(rt, n, dtype=dtype)
+        parts = _scan_aligned(v, out, add, exclusive=False, init=None)
+        exp = np.cumsum(x.astype(np.int64 if dtype == np.int32 else np.float64))
+        assert np.array_equal(out.to_numpy(), exp.astype(dtype))
+        lens = O.block_lengths(n, p)
+        offs = np.concatenate([[0], np.cumsum(lens)])
+        want = [x[offs[k]:offs[k + 1]].astype(np.int64 if dtype == np.int32 else np.float64).sum() for k in range(p)]
+        assert [float(q) for q in parts] == [float(w) for w in want]
+        sr.exclusive_scan(v, out, 7)
+        assert np.array_equal(out.to_numpy(), (7 + np.concatenate([[0], exp[:-1]])).astype(dtype))
+        assert sr.reduce(v, 0) == (int(x.astype(np.int64).sum()) if dtype == np.int32 else pytest.approx(float(exp[-1])))
+        assert sr.reduce(v, 10**9, sr.minimum) == x.min()
+
+    def test_partition_with_empty_and_ragged_segments(self, rt_pool, monkeypatch):
+        from paper_2406_00158_b200 import algorithms as A
+
+        monkeypatch.setattr(A, "_BATCH_MIN", 1)
+        x = O.mod_ints(5, 0, 100_000, 101, -50).astype(np.int64)
+        v = sr.DistributedVector.from_numpy(rt_pool(6), x, partition=[0, 40_001, 0, 7, 59_992, 0])
+        out = sr.DistributedVector.from_numpy(rt_pool(6), np.zeros_like(x), partition=[0, 40_001, 0, 7, 59_992, 0])
+        sr.inclusive_scan(v, out)
+        assert np.array_equal(out.to_numpy(), np.cumsum(x))
+        assert sr.reduce(views.transform(views.zip(v, v), lambda t: t[0] * t[1]), 0) == int((x * x).sum())
+
+    def test_dot_batched_matches_per_segment(self, rt_pool):
+        x = O.unit_doubles(9, 0, 1 << 22).astype(np.float32)
+        y = O.unit_doubles(9, 1 << 22, 1 << 22).astype(np.float32)
+        rt = rt_pool(8)
+        got = B.dot_product(sr.DistributedVector.from_numpy(rt, x), sr.DistributedVector.from_numpy(rt, y))
+        want = float(np.dot(x.astype(np.float64), y.astype(np.float64)))
+        assert abs(got - want) <= 1e-5 * abs(want)
+
+    def test_unaligned_views_fall_back(self, rt_pool, monkeypatch):
+        from paper_2406_00158_b200 import algorithms as A
+
+        monkeypatch.setattr(A, "_BATCH_MIN", 1)
+        x = O.mod_ints(6, 0, 50_001, 11, -5).astype(np.int32)
+        v = sr.DistributedVector.from_numpy(rt_pool(4), x)
+        w = views.drop(v, 3)
+        out = sr.DistributedVector(rt_pool(4), len(x) - 3, dtype=np.int32)
+        sr.inclusive_scan(w, out)
+        assert np.array_equal(out.to_numpy(), np.cumsum(x[3:].astype(np.int64)).astype(np.int32))
+        assert sr.reduce(w, 0) == int(x[3:].astype(np.int64).sum())
