@@ -198,8 +198,16 @@ def dtype_code(dtype) -> int:
         ) from None
 
 
+_ACC = {}
+
+
 def acc_dtype(dtype, op: int) -> np.dtype:
-    return CODE_DTYPE[load().drk_acc_dtype(dtype_code(dtype), op)]
+    """Accumulator dtype of the device kernels for (dtype, op) (cached drk_acc_dtype)."""
+    key = (np.dtype(dtype), op)
+    r = _ACC.get(key)
+    if r is None:
+        r = _ACC[key] = CODE_DTYPE[load().drk_acc_dtype(dtype_code(dtype), op)]
+    return r
 
 
 def scalar_buffer(value, dtype) -> ctypes.Array:

@@ -161,11 +161,18 @@ def _finish(rt, launches):
 # reduce
 
 
+_PARTIAL_DTYPE = {}
+
+
 def _partial_dtype(op: BinaryOp, dtype):
     """numpy's reduce result dtype (int32 add/mul -> int64, float32 stays float32)."""
-    if op.ufunc is not None:
-        return op.ufunc.reduce(np.zeros(1, dtype=dtype)).dtype
-    return np.dtype(dtype)
+    if op.ufunc is None:
+        return np.dtype(dtype)
+    key = (op.ufunc, np.dtype(dtype))
+    r = _PARTIAL_DTYPE.get(key)
+    if r is None:
+        r = _PARTIAL_DTYPE[key] = op.ufunc.reduce(np.zeros(1, dtype=dtype)).dtype
+    return r
 
 
 def reduce(r, init=0, op=add):

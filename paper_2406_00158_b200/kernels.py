@@ -296,6 +296,9 @@ def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
 # scan
 
 
+_SCAN_SCRATCH_BYTES = {}
+
+
 def run_scan(dtype, opcode, exclusive, in_ptr, out_ptr, n, lctx: Launch, *, init=None, carry_value=None,
              carry_dev=None, seg_total_slot=None, carry_out_slot=None, chained=False, scratch_index=0):
     """One drk_scan over a plain device buffer (the caller materialises views first).
@@ -307,7 +310,10 @@ def run_scan(dtype, opcode, exclusive, in_ptr, out_ptr, n, lctx: Launch, *, init
     code = _lib.dtype_code(T)
     A = _lib.acc_dtype(T, opcode)
     st = lctx.state
-    nbytes = int(_lib.load().drk_scan_scratch_bytes(code, opcode, n))
+    key = (code, opcode, n)
+    nbytes = _SCAN_SCRATCH_BYTES.get(key)
+    if nbytes is None:
+        nbytes = _SCAN_SCRATCH_BYTES[key] = int(_lib.load().drk_scan_scratch_bytes(code, opcode, n))
     scratch = st.scan_scratch(nbytes, scratch_index)
     init_buf = _keep(lctx, _scalar_arg(init, A)) if init is not None else None
     carry_buf = _keep(lctx, _scalar_arg(carry_value, A)) if carry_value is not None else None
