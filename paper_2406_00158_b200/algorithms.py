@@ -290,13 +290,13 @@ def _scan_entry(r, out, op, exclusive, init):
     if not o_seg:
         raise TypeError("scan output must be a segmented device range")
     if r is out or (r_seg and is_aligned(r, out)):
-        _scan_aligned(r, out, op, exclusive, init)
+        _scan_impl(r, out, op, exclusive, init, want_partials=False)
         return
     if not isinstance(out, DistributedVector):
         raise TypeError("non-aligned scan needs a DistributedVector output")
     temp = DistributedVector.like_distribution(out.runtime, out.distribution, out.dtype)
     copy(r, temp)
-    _scan_aligned(temp, out, op, exclusive, init)
+    _scan_impl(temp, out, op, exclusive, init, want_partials=False)
 
 
 def _scan_aligned(r, out, op, exclusive, init) -> list:
@@ -305,14 +305,19 @@ def _scan_aligned(r, out, op, exclusive, init) -> list:
     return _scan_impl(r, out, op, exclusive, init)
 
 
-def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list:
+def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_partials=True) -> list:
     """Aligned scan with an optional incoming carry (the fold of everything before r,
     in the accumulator type; used when r is one rank's block of a larger vector).
 
     carry_hook(total_ptrs, state) -> (carry_dev_ptr or None, carry_host_fn): the incoming
     carry produced on the device between the two passes of the multi-device schedule (the
     one-process-per-GPU scan, spmd.py); carry_host_fn() gives its value on the host after
-    the scan (for the int32 range check)."""
+    the scan (for the int32 range check).
+
+    want_partials=False (the public inclusive/exclusive_scan, which return nothing): on one
+    GPU, when no int32 carry-range check is due, the scan is left running on the stream —
+    the host does not wait for the totals, later work on the stream is ordered after it,
+    and kernels on other GPUs that read its output wait for it (kernels.stage_leaves)."""
     op = as_binary_op(op)
     in_segs = segments_of(r)
     out_segs = segments_of(out)
@@ -366,7 +371,8 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list
         if (_BATCH_SCANS and 1 < m <= _lib.SCAN_SEGS and sum(w[4].length for w in work) >= _BATCH_MIN
                 and all(w[3] % 16 == 0 and w[4].ptr() % 16 == 0 for w in work)):
             # single device, several segments: one batched launch scans them as one sequence
-            return _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry)
+            return _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry,
+                                 want_partials)
         # single device: chain the carry on the device, one pass per segment
         st.ensure_results(2 * len(work) + 2)
         prev_carry = None
@@ -380,6 +386,8 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None) -> list
                      seg_total_slot=2 * j, carry_out_slot=2 * j + 1,
                      chained=prev_carry is not None and _CHAIN_SCANS, scratch_index=j % 2)
             prev_carry = 2 * j + 1
+        if not want_partials and not _needs_range_check(T):
+            return partials  # nothing to read back: the scan stays asynchronous on its stream
         raw = st.fetch_results(2 * len(work))
         for j, (k, *_rest) in enumerate(work):
             total = np.frombuffer(raw[16 * j : 16 * j + A.itemsize].tobytes(), dtype=A)[0]
@@ -431,7 +439,14 @@ _BATCH_SCANS = True  # one drk_scan_batch launch for the segments a GPU holds (u
 _BATCH_MIN = 1 << 20  # below this many elements the chained single-pass scans are cheaper
 
 
-def _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry):
+def _needs_range_check(T):
+    """int32 scans check the carry range on the host (the reference's OverflowError)."""
+    T = np.dtype(T)
+    return T.kind in "iu" and T.itemsize < 8
+
+
+def _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry,
+                  want_partials=True):
     """The segments on one GPU scanned by one drk_scan_batch launch: the L2 scan runs over
     their concatenation, so the look-back carries the prefix from segment to segment
     (algorithms.py:256-262 without a pass per segment), and the per-segment totals — the
@@ -451,6 +466,8 @@ def _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init
                           ctypes.addressof(init_buf) if init_buf is not None else None,
                           ctypes.addressof(carry_buf) if carry_buf is not None else None, None,
                           st.result_dev_ptr(0), None, scratch.data_ptr(), scratch.numel())
+    if not want_partials and not _needs_range_check(T):
+        return partials  # nothing to read back: the scan stays asynchronous on its stream
     raw = st.fetch_results(m)
     for j, (k, *_rest) in enumerate(work):
         total = np.frombuffer(raw[8 * j: 8 * j + A.itemsize].tobytes(), dtype=A)[0]

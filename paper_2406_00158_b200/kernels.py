@@ -99,6 +99,13 @@ def stage_leaves(leaves, launch: Launch):
     from .runtime import await_pending
 
     await_pending(launch.state, [lf.handle for lf in leaves if lf.kind == "array" and lf.handle is not None])
+    # leaves on other GPUs are read over NVLink: order this launch after the work already
+    # enqueued on their devices (an asynchronous scan may still be writing them)
+    waited = set()
+    for lf in leaves:
+        if lf.kind == "array" and lf.handle is not None and lf.device != launch.device and lf.device not in waited:
+            waited.add(lf.device)
+            launch.state.stream.wait_event(lf.handle.runtime.device_state(lf.device).compute_event())
     ptrs = []
     for lf in leaves:
         if lf.kind == "array":
