@@ -151,7 +151,18 @@ def _collect_writes(result, target, writes):
     writes.append((target, result))
 
 
+# Element-wise algorithms (for_each, copy, fill, transform) return once their kernels are
+# enqueued.  Everything that reads the results is ordered after them: later work on the same
+# GPU by stream order, kernels on other GPUs by an event wait (kernels.stage_leaves), host
+# reads (to_numpy, element access, copies to host) by a stream sync, peer copies and sort by
+# an explicit sync of the source GPU.  Device temporaries are stream-ordered allocations, so
+# dropping them here is safe.  _SYNC_ALGORITHMS = True restores wait-on-return.
+_SYNC_ALGORITHMS = False
+
+
 def _finish(rt, launches):
+    if not _SYNC_ALGORITHMS:
+        return
     devs = {id(l.state): l.state for l in launches}
     for st in devs.values():
         st.synchronize()
