@@ -832,11 +832,14 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
 template <class T, class Op>
 static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
   constexpr int IT = ScanItems<T, Op>::value;
-  const int subs = g_scan_l2_subs ? g_scan_l2_subs : 8;  // 160 KB tiles (fp32/int32), 8 x 20 KB
+  // 160 KB tiles (8 x 20 KB for 4-byte types); below 2^25 elements (about one wave of
+  // tiles) 80 KB tiles, which give the grid more waves (2^23: 32.8 -> 26.9 us)
+  const int subs = g_scan_l2_subs ? g_scan_l2_subs : (n < ((int64_t)1 << 25) ? 4 : 8);
   p.pre = g_scan_l2_pre;
   switch (subs) {
-    // other tile sizes measured (7, 10, 12 sub-tiles: 0.75-0.94 of the 8-sub-tile rate) are
-    // not instantiated; 6 stays for experiments
+    // other tile sizes measured (3, 7, 10, 12 sub-tiles) are not instantiated; 6 stays for
+    // experiments
+    case 4: return launch_scan_l2dyn<T, Op, 4, IT, 3>(p, n, s);
     case 6: return launch_scan_l2dyn<T, Op, 6, IT, 3>(p, n, s);
     default: return launch_scan_l2dyn<T, Op, 8, IT, 3>(p, n, s);
   }
