@@ -208,10 +208,22 @@ def run_map(writes, leaves, n, launch: Launch):
         if m is not None:
             name, build = m
             launch_kernel(name, launch, n, *build(tgt.ptr(), n, ptrs, launch))
+            _release_peers(leaves, launch)
             return
     from . import codegen
 
     codegen.run_map(writes, leaves, ptrs, n, launch)
+    _release_peers(leaves, launch)
+
+
+def _release_peers(leaves, launch: Launch):
+    """After a kernel that reads other GPUs' memory over NVLink: their streams wait for it, so
+    nothing they run later (a write, or the reuse of freed memory) overtakes the read."""
+    done = set()
+    for lf in leaves:
+        if lf.kind == "array" and lf.handle is not None and lf.device != launch.device and lf.device not in done:
+            done.add(lf.device)
+            lf.handle.runtime.device_state(lf.device).stream.wait_event(launch.state.compute_event())
 
 
 def _dealias(writes, leaves, n, launch):
