@@ -748,3 +748,44 @@ class TestBatchedSegments:
         sr.inclusive_scan(w, out)
         assert np.array_equal(out.to_numpy(), np.cumsum(x[3:].astype(np.int64)).astype(np.int32))
         assert sr.reduce(w, 0) == int(x[3:].astype(np.int64).sum())
+
+
+class TestAsyncReturn:
+    """Element-wise algorithms and fp32 scans return before their kernels finish; every read
+    of their results must still see them (stream order, host-read syncs)."""
+
+    def test_chain_without_waits_then_host_read(self, rt_pool):
+        n = 1 << 22
+        x = O.unit_doubles(3, 0, n).astype(np.float32)
+        rt = rt_pool(3)
+        v = sr.DistributedVector.from_numpy(rt, x)
+        a = sr.DistributedVector(rt, n, dtype=np.float32)
+        b = sr.DistributedVector(rt, n, dtype=np.float32)
+        for _ in range(5):  # queue several dependent launches with no host wait in between
+            sr.transform(v, a, lambda e: e * 2.0)
+            sr.inclusive_scan(a, b)
+            sr.transform(b, a, lambda e: e - 1.0)
+        exp_b = np.cumsum((x * np.float32(2.0)).astype(np.float64))
+        np.testing.assert_allclose(b.to_numpy(), exp_b, rtol=1e-5)
+        assert a[n - 1] == np.float32(b[n - 1]) - np.float32(1.0)
+
+    def test_free_and_reallocate_after_async_write(self, rt_pool):
+        rt = rt_pool(2)
+        n = 1 << 20
+        for k in range(4):
+            v = sr.DistributedVector(rt, n, dtype=np.float32)
+            sr.fill(v, float(k))
+            w = sr.DistributedVector(rt, n, dtype=np.float32)
+            sr.copy(v, w)
+            del v  # freed while the copy may still be reading it (stream-ordered reuse)
+            u = sr.DistributedVector(rt, n, dtype=np.float32)
+            sr.fill(u, -1.0)
+            assert (w.to_numpy() == float(k)).all()
+            assert (u.to_numpy() == -1.0).all()
+
+    def test_reduce_after_async_writes(self, rt_pool):
+        rt = rt_pool(4)
+        v = sr.DistributedVector(rt, 1_000_003, dtype=np.int64)
+        sr.fill(v, 3)
+        sr.transform(v, v, lambda e: e * 7)
+        assert sr.reduce(v, 0) == 21 * 1_000_003
