@@ -146,6 +146,7 @@ static int g_scan_l2_subs = 0;   // sub-tiles per L2 tile (0: 8 = 160 KB for 4-b
 static int g_scan_l2_pre = 2;    // sub-tiles scanned prefix-free during the look-back
 static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
 static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
+static int g_scan_stagger = -1;  // ns between first-wave tile starts of the L2 scan (-1: automatic)
 static thread_local int g_chain_launch = 0;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
 static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
                                  // measured slower than one 120 KB tile per CTA
@@ -177,6 +178,9 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2_pre")) {
     old = g_scan_l2_pre;
     g_scan_l2_pre = value;
+  } else if (!strcmp(name, "scan_stagger")) {
+    old = g_scan_stagger;
+    g_scan_stagger = value;
   } else if (!strcmp(name, "scan_debug")) {
     old = g_scan_debug;
     g_scan_debug = value;
@@ -808,7 +812,13 @@ static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>
     // before it, whose scratch the successor reuses.
     int dev = 0;
     cudaGetDevice(&dev);
-    p2.early_trigger = nt > 2 * (int64_t)sm_count(dev) * occupancy(k, BLOCK, smem);
+    const int64_t wave = (int64_t)sm_count(dev) * occupancy(k, BLOCK, smem);
+    p2.early_trigger = nt > 2 * wave;
+    // Stagger the first wave's reduces (ticket order) when the grid spans several waves:
+    // 2^26-2^28 elements gain 4-6 %; a single wave gains nothing (all tiles must be read
+    // before the last look-back resolves anyway)
+    p2.stagger_tiles = (u32)wave;
+    if (g_scan_stagger < 0) p2.stagger_ns = nt > 2 * wave ? 40 : 0;
     if (g_chain_launch) {
       // programmatic dependent of the previous scan of the chain (see carry_dev_read)
       cudaLaunchConfig_t cfg = {};
@@ -889,6 +899,8 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   p.carry_out = (A*)carry_out;
   p.counter = (u32*)b;
   p.desc = (u64*)(b + 128);
+  p.t0slot = (u64*)(b + 64);
+  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;  // < 0: automatic (launch_scan_l2dyn)
   p.epoch = next_epoch(scratch);
   p.bulk_ok = aligned16(in) && aligned16(out);
   p.trace = (u64*)g_scan_trace;
