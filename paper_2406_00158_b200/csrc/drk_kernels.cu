@@ -1056,6 +1056,10 @@ static int launch_scan_batch(int exclusive, int nseg, const void* const* ins, vo
   const int smem = 3 * BLOCK * IT * (int)sizeof(T);
   auto k = scan_l2_kernel<T, Op, BLOCK, IT, SUBS, false, 3>;
   DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int64_t wave = (int64_t)sm_count(device) * occupancy(k, BLOCK, smem);
+  p.t0slot = (u64*)(b + 64);
+  p.stagger_tiles = (u32)wave;
+  p.stagger_ns = g_scan_stagger >= 0 ? (u32)g_scan_stagger : ((int64_t)nt > 2 * wave ? 40u : 0u);
   k<<<(unsigned)nt, BLOCK, smem, (cudaStream_t)stream>>>(p);
   if (seg_totals) seg_totals_kernel<T, Op><<<nseg, 256, 0, (cudaStream_t)stream>>>(p.aggs, p, (char*)seg_totals);
   return epilogue(what);
