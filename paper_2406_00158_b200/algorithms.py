@@ -31,6 +31,32 @@ from .runtime import AggregateTaskError
 from .views import ReadOnly, Target, ZipView, lower
 
 
+# Tracing: DRK_NVTX=1 wraps every public algorithm in an NVTX range named after
+# it, so an nsys / Nsight timeline shows the algorithm calls above their kernels.  Off by
+# default (no cost beyond one flag test).
+import functools
+import os as _os
+
+_NVTX = _os.environ.get("DRK_NVTX") == "1"
+
+
+def _traced(fn):
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        if not _NVTX:
+            return fn(*args, **kwargs)
+        from .runtime import torch
+
+        nvtx = torch().cuda.nvtx
+        nvtx.range_push("drk." + fn.__name__)
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            nvtx.range_pop()
+
+    return wrapper
+
+
 @dataclass(frozen=True)
 class BinaryOp:
     """A binary operator with optional identity and numpy ufunc (algorithms.py:34-44)."""
@@ -103,6 +129,7 @@ def _promote_python(value):
 # for_each
 
 
+@_traced
 def for_each(r, fn, vectorized: bool = False) -> None:
     """Apply fn to every element; its non-None result replaces the element (a tuple for
     zips, None components skipped).  Effects are visible on return (algorithms.py:86-98)."""
@@ -186,6 +213,7 @@ def _partial_dtype(op: BinaryOp, dtype):
     return r
 
 
+@_traced
 def reduce(r, init=0, op=add):
     """Fold all elements onto init: per-segment device partials, then an ascending fold on
     the driver (algorithms.py:135-150), so exact types give identical results for every
@@ -284,11 +312,13 @@ def _batch_reduce(rt, lowered, opcode):
 # scans
 
 
+@_traced
 def inclusive_scan(r, out, op=add) -> None:
     """out[i] = fold of r[0..i] (algorithms.py:169-177)."""
     _scan_entry(r, out, as_binary_op(op), exclusive=False, init=None)
 
 
+@_traced
 def exclusive_scan(r, out, init, op=add) -> None:
     """out[0] = init, out[i] = init ⊕ fold of r[0..i) (algorithms.py:180-182)."""
     _scan_entry(r, out, as_binary_op(op), exclusive=True, init=init)
@@ -607,6 +637,7 @@ def _check_carry_range(op, partials, live, exclusive, init, T, carry=None):
 # sort
 
 
+@_traced
 def sort(r, key=None, *, strategy: str | None = None) -> None:
     """In-place ascending sort of a distributed vector (algorithms.py:315-432); with `key`,
     a stable sort by key(x) (the key function is traced like any element function).
@@ -724,6 +755,7 @@ class _DeviceTarget(Target):
 # copy / fill / transform
 
 
+@_traced
 def copy(src, dst) -> None:
     """Element copy between equal-length ranges: aligned pairs segment by segment, else
     chunks at the union of both sides' boundaries (algorithms.py:468-503).  Sources may
@@ -783,11 +815,13 @@ def _copy_to_host(rt, ls, piece, launches):
     host[...] = tmp.cpu().numpy()
 
 
+@_traced
 def fill(r, value) -> None:
     """Set every element of a writable range to value."""
     for_each(r, lambda _x: value, vectorized=True)
 
 
+@_traced
 def transform(src, dst, fn) -> None:
     """dst[i] = fn(src[i]) — the reference spells this copy(views.transform(src, fn), dst)
     (algorithms.py:468-503, tests/test_algorithms.py:376-381)."""

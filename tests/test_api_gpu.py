@@ -789,3 +789,16 @@ class TestAsyncReturn:
         sr.fill(v, 3)
         sr.transform(v, v, lambda e: e * 7)
         assert sr.reduce(v, 0) == 21 * 1_000_003
+
+
+def test_nvtx_ranges_do_not_change_results(rt_pool, monkeypatch):
+    from paper_2406_00158_b200 import algorithms as A
+
+    monkeypatch.setattr(A, "_NVTX", True)
+    x = np.arange(1, 10_001, dtype=np.int64)
+    v = sr.DistributedVector.from_numpy(rt_pool(3), x)
+    out = sr.DistributedVector(rt_pool(3), len(x), dtype=np.int64)
+    sr.inclusive_scan(v, out)
+    sr.transform(out, out, lambda e: e * 2)
+    assert sr.reduce(v, 0) == int(x.sum())
+    assert np.array_equal(out.to_numpy(), 2 * np.cumsum(x))
