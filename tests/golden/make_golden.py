@@ -169,6 +169,19 @@ def main():
                     parts = A._scan_aligned(v, out, getattr(A, opname), exclusive=False, init=None)
                     add_case({"op": "inclusive_scan", "ufunc": opname, "dtype": dt, "n": n, "p": p, "init": None,
                               "inputs": [d], "partials": [enc(q) for q in parts]}, out.to_numpy())
+    # exclusive scans with minimum / maximum (init takes part in every prefix)
+    for opname, dt, init in (("minimum", "int32", 0), ("maximum", "float64", 0.25), ("minimum", "float32", 0.5)):
+        for n in (17, 1000, 4099):
+            for p in (1, 3, 7):
+                d = ({"kind": "mod", "seed": 10, "start": 0, "n": n, "modulus": 2001, "offset": -1000}
+                     if dt == "int32" else {"kind": "unit", "seed": 10, "start": 0, "n": n})
+                x = gen(d, dt)
+                v = DistributedVector.from_numpy(rts[p], x)
+                out = DistributedVector(rts[p], n, init=0, dtype=np.dtype(dt))
+                parts = A._scan_aligned(v, out, getattr(A, opname), exclusive=True, init=init)
+                add_case({"op": "exclusive_scan", "ufunc": opname, "dtype": dt, "n": n, "p": p, "init": enc(init),
+                          "inputs": [d], "partials": [enc(q) for q in parts]}, out.to_numpy())
+
     # int32 carry overflow raises (algorithms.py:292-296 -> np.add(off, int32) OverflowError)
     n = 4096
     d = {"kind": "mod", "seed": 1, "start": 0, "n": n, "modulus": 1, "offset": 1_000_000}
