@@ -147,12 +147,33 @@ int drk_scan_ex(int dtype, int op, int exclusive, int flags, const void* in, voi
                 const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total_dev,
                 void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream);
 
+/* Scan of a fused view (algorithms.py:198-202 + views.py:164-181 without the temporary):
+ * out = scan(f(leaves)) reading only the view's leaves.  `words` (nwords <= 16) describe the
+ * view in 8-byte words:
+ *   DRK_VIEW_PRODUCT  f = x[i] * y[i]            words {x, y}                (one rounding)
+ *   DRK_VIEW_AFFINE   f = alpha * x[i] (+ beta)  words {x, bits(alpha), bits(beta), 1 if beta}
+ * (constants as bit patterns in dtype).  vec_ok = every leaf 16-byte aligned; with out also
+ * 16-byte aligned and n large the L2 two-touch kernel runs, else the single-pass kernel.
+ * op must be DRK_ADD (other operators: NVRTC, drk_jit_scan_view).  Other arguments and the
+ * scratch (drk_scan_scratch_bytes) as drk_scan; flags as drk_scan_ex. */
+enum { DRK_VIEW_PRODUCT = 1, DRK_VIEW_AFFINE = 2 };
+int drk_scan_view(int kind, int dtype, int op, int exclusive, const uint64_t* words, int nwords, int vec_ok,
+                  void* out, int64_t n, const void* init_host, const void* carry_host, const void* carry_dev,
+                  void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,
+                  void* stream);
+int drk_scan_view_ex(int kind, int dtype, int op, int exclusive, int flags, const uint64_t* words, int nwords,
+                     int vec_ok, void* out, int64_t n, const void* init_host, const void* carry_host,
+                     const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
+                     size_t scratch_bytes, int device, void* stream);
+
 /* Batched segment scan: the nseg (<= DRK_SCAN_SEGS) segments of a vector that live on one GPU
- * — ins[k] -> outs[k], ns[k] >= 1 elements, 16-byte aligned — scanned in one launch as one
- * sequence (algorithms.py:234-308 with the carries between them folded by the look-back),
- * starting from carry_host or carry_dev.  seg_totals_dev (nullable) receives each segment's
- * own total in 8-byte slots (accumulator type), carry_out_dev (nullable) the carry after the
- * last segment.  Scratch: drk_scan_batch_scratch_bytes (zeroed once, reusable). */
+ * — ins[k] -> outs[k], ns[k] >= 1 elements, 16-byte aligned — scanned in one launch
+ * (algorithms.py:234-308): segment k starts from C_k = carry ⊕ L(T_0) ⊕ .. ⊕ L(T_{k-1}),
+ * the segment totals T rounded to numpy's accumulate dtype like the reference's driver fold,
+ * passed on the device from the last tile of segment k-1; the first segment starts from
+ * carry_host or carry_dev.  seg_totals_dev (nullable) receives each segment's own total in
+ * 8-byte slots (accumulator type), carry_out_dev (nullable) C_nseg.  Scratch:
+ * drk_scan_batch_scratch_bytes (zeroed once, reusable). */
 #define DRK_SCAN_SEGS 16
 size_t drk_scan_batch_scratch_bytes(int dtype, int op, int nseg, const int64_t* ns);
 int drk_scan_batch(int dtype, int op, int exclusive, int nseg, const void* const* ins, void* const* outs,
@@ -222,6 +243,13 @@ int drk_jit_scan(void* handle, const char* kernel, int acc_bytes, int tile, int 
                  const void* in, void* out, int64_t n, const void* init_host, const void* carry_host,
                  const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
                  size_t scratch_bytes, int device, void* stream);
+/* scan of a fused view with an NVRTC module that defines drk_scan_l2_4, drk_scan_l2_8 and
+ * drk_scan_1p over its generated loader (value size v_bytes, accumulator size acc_bytes):
+ * arguments as drk_scan_view_ex; scratch of drk_jit_scan_scratch_bytes(n, 256 * items). */
+int drk_jit_scan_view(void* handle, int v_bytes, int acc_bytes, int exclusive, int flags, const uint64_t* words,
+                      int nwords, int vec_ok, void* out, int64_t n, const void* init_host, const void* carry_host,
+                      const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
+                      size_t scratch_bytes, int device, void* stream);
 const char* drk_jit_last_error(void);
 int64_t drk_note_launch(void);
 

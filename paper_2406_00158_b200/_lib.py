@@ -85,6 +85,12 @@ SIGNATURES = {
     "drk_scan_batch": (_int, [_int, _int, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64),
                               _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "drk_scan_ex": (_int, [_int, _int, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
+    "drk_scan_view": (_int, [_int, _int, _int, _int, ctypes.POINTER(_u64), _int, _int, _vp, _i64, _vp, _vp, _vp, _vp,
+                             _vp, _vp, _sz, _int, _vp]),
+    "drk_scan_view_ex": (_int, [_int, _int, _int, _int, _int, ctypes.POINTER(_u64), _int, _int, _vp, _i64, _vp, _vp,
+                                _vp, _vp, _vp, _vp, _sz, _int, _vp]),
+    "drk_jit_scan_view": (_int, [_vp, _int, _int, _int, _int, ctypes.POINTER(_u64), _int, _int, _vp, _i64, _vp, _vp,
+                                 _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "drk_carry_fold": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _vp, _vp, _vp, _int,
                               _vp]),
     "drk_sort_keys": (_int, [_int, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
@@ -176,6 +182,8 @@ CARRY_MAX = 64  # drk.h DRK_CARRY_MAX: predecessors one drk_carry_fold call fold
 SCAN_CHAINED = 1  # drk.h DRK_SCAN_CHAINED
 SCAN_SEGS = 16  # drk.h DRK_SCAN_SEGS
 RED_SEGS = 16  # drk.h DRK_RED_SEGS
+VIEW_PRODUCT, VIEW_AFFINE = 1, 2  # drk.h DRK_VIEW_*
+JIT_WORDS = 16  # drk_device.cuh DRK_JIT_WORDS: 8-byte words of a fused scan loader
 
 # sort / gather / bounds also take unsigned keys (drk.h DRK_U32 / DRK_U64)
 SORT_DTYPE_CODE = {**DTYPE_CODE, np.dtype(np.uint32): 4, np.dtype(np.uint64): 5}

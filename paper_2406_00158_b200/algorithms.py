@@ -373,8 +373,9 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
 
         return codegen.custom_scan(rt, in_segs, out_segs, live, op, exclusive, init, carry)
 
-    # 1. bring every live input segment into its output segment's dtype/buffer if it is a
-    #    view (materialise into `out`, then scan in place); plain vectors scan in -> out.
+    # 1. what each live segment scan reads: a plain device array in the output dtype, or a
+    #    view — fused into the scan kernel (its leaves are read, nothing is materialised;
+    #    the reference materialises f's result, views.py:164-181, then accumulates it)
     work = []
     launches = {}
     for k in live:
@@ -392,11 +393,13 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
             from .runtime import await_pending
 
             await_pending(st, [lw.leaves[node.value].handle, tgt.handle])
-            in_ptr = lw.leaves[node.value].ptr()
+            src = lw.leaves[node.value].ptr()
         else:
-            run_map([(tgt, node)], lw.leaves, lw.length, launch)
-            in_ptr = tgt.ptr()
-        work.append((k, st, launch, in_ptr, tgt))
+            src = _fused_scan_source(node, lw, tgt, opcode, launch)
+            if src is None:
+                run_map([(tgt, node)], lw.leaves, lw.length, launch)
+                src = tgt.ptr()
+        work.append((k, st, launch, src, tgt))
 
     T = np.dtype(out.dtype if hasattr(out, "dtype") else work[0][4].dtype)
     A = _lib.acc_dtype(T, opcode)
@@ -410,7 +413,7 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
         st = work[0][1]
         m = len(work)
         if (_BATCH_SCANS and 1 < m <= _lib.SCAN_SEGS and sum(w[4].length for w in work) >= _BATCH_MIN
-                and all(w[3] % 16 == 0 and w[4].ptr() % 16 == 0 for w in work)):
+                and all(isinstance(w[3], int) and w[3] % 16 == 0 and w[4].ptr() % 16 == 0 for w in work)):
             # single device, several segments: one batched launch scans them as one sequence
             return _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init, init_a, carry,
                                  want_partials)
@@ -421,11 +424,11 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
             first_carry = _to_acc(carry, A) if (j == 0 and carry is not None) else None
             # segment j's carry is written by segment j-1's scan, enqueued just before: chain
             # them (programmatic dependent launch) so j's tiles reduce while j-1 drains
-            run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a,
-                     carry_value=first_carry,
-                     carry_dev=st.result_dev_ptr(prev_carry) if prev_carry is not None else None,
-                     seg_total_slot=2 * j, carry_out_slot=2 * j + 1,
-                     chained=prev_carry is not None and _CHAIN_SCANS, scratch_index=j % 2)
+            _run_segment_scan(T, opcode, exclusive, in_ptr, tgt, launch, init=init_a,
+                              carry_value=first_carry,
+                              carry_dev=st.result_dev_ptr(prev_carry) if prev_carry is not None else None,
+                              seg_total_slot=2 * j, carry_out_slot=2 * j + 1,
+                              chained=prev_carry is not None and _CHAIN_SCANS, scratch_index=j % 2)
             prev_carry = 2 * j + 1
         if not want_partials and not _needs_range_check(T):
             return partials  # nothing to read back: the scan stays asynchronous on its stream
@@ -451,8 +454,7 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
     for k, st, launch, in_ptr, tgt in work:
         slot = per_dev_slot.get(id(st), 0)
         per_dev_slot[id(st)] = slot + 1
-        kernels.launch_kernel("drk_reduce", launch, tgt.length, _lib.dtype_code(T), opcode, in_ptr, tgt.length,
-                       st.host_result_dev_ptr(slot), st.reduce_scratch.data_ptr())
+        _segment_total(T, opcode, in_ptr, tgt, launch, st.host_result_dev_ptr(slot))
     fetched = {id(w[1]): w[1].fetch_host_results(per_dev_slot[id(w[1])]) for w in work}
     counter = {}
     for k, st, *_ in work:
@@ -464,8 +466,8 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
     _check_carry_range(op, partials, live, exclusive, init, T, carry)
     for k, st, launch, in_ptr, tgt in work:
         off = offsets[k]
-        run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a,
-                 carry_value=_to_acc(off, A) if off is not None else None)
+        _run_segment_scan(T, opcode, exclusive, in_ptr, tgt, launch, init=init_a,
+                          carry_value=_to_acc(off, A) if off is not None else None)
     for l in launches.values():
         l.state.synchronize()
     return partials
@@ -541,8 +543,7 @@ def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, ini
         slot = used.get(id(st), 0)
         used[id(st)] = slot + 1
         tot_ptr[k] = st.result_dev_ptr(slot)
-        kernels.launch_kernel("drk_reduce", launch, tgt.length, code, opcode, in_ptr, tgt.length, tot_ptr[k],
-                              st.reduce_scratch.data_ptr())
+        _segment_total(T, opcode, in_ptr, tgt, launch, tot_ptr[k])
     reduced = {}
     for k, st, *_ in work:
         if id(st) not in reduced:
@@ -580,7 +581,7 @@ def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, ini
             carry_dev = st.result_dev_ptr(cslot)
             kernels.launch_kernel("drk_carry_fold", launch, 1, code, opcode, vals, None, len(before),
                                   ctypes.addressof(carry_buf) if carry_buf is not None else None, in_dev, carry_dev)
-        run_scan(T, opcode, exclusive, in_ptr, tgt.ptr(), tgt.length, launch, init=init_a, carry_dev=carry_dev)
+        _run_segment_scan(T, opcode, exclusive, in_ptr, tgt, launch, init=init_a, carry_dev=carry_dev)
     raw = {}
     for k, st, *_ in work:
         if id(st) not in raw:
@@ -597,6 +598,51 @@ def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, ini
         carry = carry_host_fn()
     _check_carry_range(op, partials, live, exclusive, init, T, carry)
     return partials
+
+
+# Views scanned in a fused kernel (kernels.run_scan_view); False materialises them first.
+_FUSE_SCAN_VIEWS = True
+
+
+def _fused_scan_source(node, lw, tgt, opcode, launch):
+    """A view input of a segment scan as a kernels.ScanView (its value cast to the output
+    dtype, like store_array's cast, then scanned), or None to materialise it instead (fusion
+    off, or an expression the fused loader cannot take)."""
+    if not _FUSE_SCAN_VIEWS or tgt.dtype not in _lib.DTYPE_CODE:
+        return None
+    from . import codegen
+
+    node_t = expr.cast(node, tgt.dtype)
+    leaves = kernels._dealias([(tgt, node_t)], lw.leaves, lw.length, launch)
+    if kernels.match_scan_view(node_t, leaves, opcode, tgt.dtype) is None:
+        try:  # compile (or fetch) the NVRTC loader now, so a failure can fall back
+            probe = kernels.ScanView(node_t, leaves, [0] * len(leaves), lw.length)
+            codegen.scan_view_plan(probe, tgt.dtype, opcode)
+        except codegen.JitError:
+            return None
+    from .runtime import await_pending
+
+    await_pending(launch.state, [tgt.handle])
+    ptrs = kernels.stage_leaves(leaves, launch)
+    return kernels.ScanView(node_t, leaves, ptrs, lw.length)
+
+
+def _run_segment_scan(T, opcode, exclusive, src, tgt, launch, **kw):
+    if isinstance(src, kernels.ScanView):
+        kernels.run_scan_view(T, opcode, exclusive, src, tgt.ptr(), tgt.length, launch, **kw)
+    else:
+        run_scan(T, opcode, exclusive, src, tgt.ptr(), tgt.length, launch, **kw)
+
+
+def _segment_total(T, opcode, src, tgt, launch, result_ptr):
+    """The total of one segment's input (the first pass of the multi-device scan) into the
+    device address result_ptr, in the scan's accumulator type."""
+    if isinstance(src, kernels.ScanView):
+        kernels.run_reduce(src.node, src.leaves, src.n, opcode, None, launch, 0, ptrs=src.ptrs,
+                           result_ptr=result_ptr)
+    else:
+        kernels.launch_kernel("drk_reduce", launch, tgt.length, _lib.dtype_code(T), opcode, src, tgt.length,
+                              result_ptr, launch.state.reduce_scratch.data_ptr())
 
 
 def _to_acc(v, A):

@@ -173,15 +173,44 @@ def rel_close(actual, expected, tol) -> bool:
     return bool(np.isclose(np.asarray(actual), np.asarray(expected), rtol=tol, atol=0.0).all())
 
 
-def _timed(reps, kernel, reset=None):
-    seconds, result = [], None
+def _timed(reps, kernel, rt, reset=None):
+    """Per rep: wall seconds from the call until every device stream has drained (the
+    algorithms may return once their kernels are enqueued), and device seconds from CUDA
+    events recorded on every device stream around the call (max over devices)."""
+    from .runtime import torch
+
+    t = torch()
+    seconds, device_seconds, result = [], [], None
+    states = rt.device_states
     for _ in range(reps):
         if reset is not None:
             reset()
+            rt.synchronize()
+        evs = []
+        for st in states:
+            e0, e1 = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+            e0.record(st.stream)
+            evs.append((e0, e1, st))
         t0 = time.perf_counter()
         result = kernel()
+        for e0, e1, st in evs:
+            e1.record(st.stream)
+        rt.synchronize()
         seconds.append(time.perf_counter() - t0)
-    return seconds, result
+        device_seconds.append(max(e0.elapsed_time(e1) for e0, e1, _ in evs) / 1e3)
+    return seconds, device_seconds, result
+
+
+def _gpu_extra(res, rt, device_seconds, bytes_per_elem):
+    """GPU columns of the CSV: device time, algorithmic GB/s and elements/s, fraction of the
+    aggregate HBM roofline of the GPUs the locales occupy."""
+    res.extra["device_seconds"] = list(device_seconds)
+    res.extra["bytes_per_element"] = bytes_per_elem
+    res.extra["devices"] = len(rt.device_states)
+
+
+def _dt(spec):
+    return np.dtype(spec.dtype)
 
 
 def _dt(spec):
@@ -194,8 +223,9 @@ def bench_dot(spec: BenchSpec, rt: Runtime) -> BenchResult:
     ys = repro.unit_doubles(spec.seed, n, n).astype(dt)
     x = DistributedVector.from_numpy(rt, xs)
     y = DistributedVector.from_numpy(rt, ys)
-    seconds, value = _timed(spec.reps, lambda: dot_product(x, y))
+    seconds, dsec, value = _timed(spec.reps, lambda: dot_product(x, y), rt)
     res = BenchResult(spec, seconds, repro.checksum(np.float64(value)))
+    _gpu_extra(res, rt, dsec, 2 * dt.itemsize)
     if spec.check:
         tol = REL_TOL if dt == np.float64 else 1e-5
         res.verified = rel_close(value, _oracle_dot(xs, ys), tol) if n else value == 0.0
@@ -207,8 +237,9 @@ def bench_reduce(spec: BenchSpec, rt: Runtime) -> BenchResult:
     v = DistributedVector(rt, n, dtype=np.int64)
     if n:
         algorithms.copy(views.iota(n), v)
-    seconds, value = _timed(spec.reps, lambda: algorithms.reduce(v, 0, add))
+    seconds, dsec, value = _timed(spec.reps, lambda: algorithms.reduce(v, 0, add), rt)
     res = BenchResult(spec, seconds, repro.checksum(np.int64(value)))
+    _gpu_extra(res, rt, dsec, 8)
     if spec.check:
         res.verified = value == n * (n - 1) // 2
     return res
@@ -220,9 +251,10 @@ def bench_inclusive_scan(spec: BenchSpec, rt: Runtime) -> BenchResult:
     if n:
         algorithms.copy(views.iota(n), v)
     out = DistributedVector(rt, n, init=0, dtype=np.int64)
-    seconds, _ = _timed(spec.reps, lambda: algorithms.inclusive_scan(v, out, add))
+    seconds, dsec, _ = _timed(spec.reps, lambda: algorithms.inclusive_scan(v, out, add), rt)
     data = out.to_numpy()
     res = BenchResult(spec, seconds, repro.checksum(data))
+    _gpu_extra(res, rt, dsec, 16)
     if spec.check:
         i = np.arange(n, dtype=np.int64)
         res.verified = bool(np.array_equal(data, i * (i + 1) // 2))
@@ -235,10 +267,11 @@ def bench_black_scholes(spec: BenchSpec, rt: Runtime) -> BenchResult:
             for k, (name, (lo, hi)) in enumerate(BS_RANGES.items())}
     vecs = {k: DistributedVector.from_numpy(rt, v) for k, v in cols.items()}
     out = DistributedVector(rt, n, dtype=dt)
-    seconds, _ = _timed(spec.reps, lambda: black_scholes_prices(
-        out, vecs["spot"], vecs["strike"], vecs["rate"], vecs["volatility"], vecs["expiry"]))
+    seconds, dsec, _ = _timed(spec.reps, lambda: black_scholes_prices(
+        out, vecs["spot"], vecs["strike"], vecs["rate"], vecs["volatility"], vecs["expiry"]), rt)
     data = out.to_numpy()
     res = BenchResult(spec, seconds, repro.checksum(data))
+    _gpu_extra(res, rt, dsec, 6 * dt.itemsize)
     if spec.check:
         exp = np.array([_oracle_bs(*(float(cols[k][i]) for k in BS_RANGES)) for i in range(n)])
         res.verified = rel_close(data, exp, REL_TOL if dt == np.float64 else 1e-5)
@@ -252,9 +285,10 @@ def bench_stream(spec: BenchSpec, rt: Runtime) -> BenchResult:
     a = DistributedVector(rt, n, dtype=dt)
     b = DistributedVector.from_numpy(rt, bs)
     c = DistributedVector.from_numpy(rt, cs)
-    seconds, _ = _timed(spec.reps, lambda: stream_triad(a, b, c))
+    seconds, dsec, _ = _timed(spec.reps, lambda: stream_triad(a, b, c), rt)
     data = a.to_numpy()
     res = BenchResult(spec, seconds, repro.checksum(data))
+    _gpu_extra(res, rt, dsec, 3 * dt.itemsize)
     med = sorted(seconds)[len(seconds) // 2]
     res.extra["bytes_per_second"] = 3.0 * dt.itemsize * n / med if med > 0 else float("inf")
     if spec.check:
@@ -272,9 +306,10 @@ def bench_sort(spec: BenchSpec, rt: Runtime) -> BenchResult:
     def reset():
         algorithms.copy(keys, v)
 
-    seconds, _ = _timed(spec.reps, lambda: algorithms.sort(v), reset=reset)
+    seconds, dsec, _ = _timed(spec.reps, lambda: algorithms.sort(v), rt, reset=reset)
     data = v.to_numpy()
     res = BenchResult(spec, seconds, repro.checksum(data))
+    _gpu_extra(res, rt, dsec, None)  # a sort has no single algorithmic byte count
     if spec.check:
         res.verified = bool(np.array_equal(data, np.sort(keys)))
     return res
@@ -301,17 +336,47 @@ def run_spec(spec: BenchSpec) -> BenchResult:
 
 
 CSV_HEADER = "bench,size,locales,rep,seconds,checksum,verified"
+# appended after the reference's columns (drbench --gpu-columns), so the first seven fields
+# keep the reference schema (bench.py:369-386)
+GPU_COLUMNS = "device_seconds,gbps,elements_per_second,roofline_frac,devices"
 
 
-def csv_rows(results) -> list:
-    rows = [CSV_HEADER]
+def hbm_peak_gbs() -> float:
+    """Per-GPU HBM roofline: MEASURED_PEAKS.json hbm_gbs (driver-written), else the
+    B200_PROFILING.md fallback."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6650.0
+
+
+def csv_rows(results, gpu_columns: bool = False) -> list:
+    rows = [CSV_HEADER + ("," + GPU_COLUMNS if gpu_columns else "")]
+    peak = hbm_peak_gbs() if gpu_columns else None
     for r in results:
+        dsec = r.extra.get("device_seconds", [])
+        bpe = r.extra.get("bytes_per_element")
+        ndev = r.extra.get("devices", 1)
         for i, sec in enumerate(r.seconds):
             verified = "" if r.verified is None else ("true" if r.verified else "false")
-            rows.append(f"{r.spec.name},{r.spec.size},{r.spec.locales},{i},{sec:.9f},{r.checksum},{verified}")
+            row = f"{r.spec.name},{r.spec.size},{r.spec.locales},{i},{sec:.9f},{r.checksum},{verified}"
+            if gpu_columns:
+                d = dsec[i] if i < len(dsec) else float("nan")
+                if bpe is not None and d > 0:
+                    gbps = bpe * r.spec.size / d / 1e9
+                    row += f",{d:.9f},{gbps:.3f},{r.spec.size / d:.6e},{gbps / (peak * ndev):.4f},{ndev}"
+                else:
+                    eps = r.spec.size / d if d > 0 else float("nan")
+                    row += f",{d:.9f},,{eps:.6e},,{ndev}"
+            rows.append(row)
     return rows
 
 
-def emit_csv(results, path) -> None:
+def emit_csv(results, path, gpu_columns: bool = False) -> None:
     with open(path, "w", encoding="ascii") as fh:
-        fh.write("\n".join(csv_rows(results)) + "\n")
+        fh.write("\n".join(csv_rows(results, gpu_columns)) + "\n")

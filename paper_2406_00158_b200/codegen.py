@@ -486,7 +486,7 @@ def match_binary(fn, dtype):
     return None
 
 
-def run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot):
+def run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot, result_ptr=None):
     V = np.dtype(node.dtype)
     fk = expr._fn_key(combiner.fn) if (opcode is None and combiner is not None) else None
     cacheable = opcode is not None or fk is not None
@@ -506,7 +506,7 @@ def run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot):
     vec_ok = all(ptrs[k] % 16 == 0 for k in array_slots)
     st = launch.state
     scratch = st.reduce_scratch.data_ptr()
-    res = st.host_result_dev_ptr(slot)
+    res = result_ptr if result_ptr is not None else st.host_result_dev_ptr(slot)
     blob = (words.pack() + struct.pack("<qi4x", n, 1 if vec_ok else 0)
             + struct.pack("<QQQ", scratch, scratch + 128, scratch + 128 + 4096 * 8)
             + struct.pack("<QQ", res, 0))
@@ -620,61 +620,223 @@ extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan(
 
 
 def custom_scan(rt, in_segs, out_segs, live, op, exclusive, init, carry=None):
-    """Aligned scan with an operator that is not a numpy ufunc (algorithms.py:216-231,
-    `functools`-style Python fold).  Inputs are materialised into the output segments,
-    then scanned in place with a generated scan kernel; carries chain on the device."""
-    from .kernels import Launch, run_map
+    """Aligned scan with an operator that is not a numpy ufunc (algorithms.py:216-231, the
+    Python fold of `_accumulate`).  If the traced operator is exactly add / multiply /
+    minimum / maximum of its arguments, the libdrk scans run.  Otherwise each segment is
+    scanned by a generated kernel that applies the traced combiner — reading a plain vector
+    directly, or a view fused into the scan (no materialised input).  One GPU: the carry
+    chains on the device.  Several GPUs: every segment's total is reduced on its GPU with
+    the same combiner, the host folds the totals in segment order exactly like the
+    reference's driver loop (algorithms.py:256-262), and each segment is scanned with its
+    carry."""
+    from .algorithms import BinaryOp, _scan_impl
+    from .kernels import Launch, ScanView, run_reduce, run_scan_view, stage_leaves, _dealias
+    from .runtime import await_pending
     from .views import Target, lower
 
     T = None
-    work = []
     for k in live:
-        lw = lower(in_segs[k])
         tgt = lower(out_segs[k]).target
         if not isinstance(tgt, Target):
             raise TypeError("scan output segments must be writable vector storage")
         T = np.dtype(tgt.dtype)
-        st = rt.state_of(out_segs[k].rank)
-        launch = Launch(st)
-        run_map([(tgt, lw.value)], lw.leaves, lw.length, launch)
-        work.append((k, st, launch, tgt))
     code = match_binary(op.fn, T)
     if code is not None:
-        from .algorithms import BinaryOp, _scan_impl
-
         ufunc = {_lib.ADD: np.add, _lib.MUL: np.multiply, _lib.MIN: np.minimum, _lib.MAX: np.maximum}[code]
-        return _scan_impl(out_segs_view(out_segs), out_segs_view(out_segs), BinaryOp(op.fn, op.identity, ufunc),
-                          exclusive, init, carry)
+        return _scan_impl(_SegList(in_segs), out_segs_view(out_segs), BinaryOp(op.fn, op.identity, ufunc), exclusive,
+                          init, carry)
     mod, items = scan_module(T, op)
     tile = BLOCK * items
+    work = []
+    for k in live:
+        lw = lower(in_segs[k])
+        tgt = lower(out_segs[k]).target
+        st = rt.state_of(out_segs[k].rank)
+        launch = Launch(st)
+        node = lw.value
+        if isinstance(node, tuple):
+            raise TypeError("scan needs scalar elements; apply a transform to the zip first")
+        plain = node.op == "leaf" and lw.leaves[node.value].kind == "array" and node.dtype == T
+        if plain and lw.leaves[node.value].device == st.index:
+            await_pending(st, [lw.leaves[node.value].handle, tgt.handle])
+            node_t = node
+            leaves = lw.leaves
+            ptrs = [lf.ptr() if lf.kind == "array" else 0 for lf in leaves]
+            src = leaves[node.value].ptr()
+        else:
+            node_t = expr.cast(node, T)
+            leaves = _dealias([(tgt, node_t)], lw.leaves, lw.length, launch)
+            await_pending(st, [tgt.handle])
+            ptrs = stage_leaves(leaves, launch)
+            src = ScanView(node_t, leaves, ptrs, lw.length)
+        work.append((k, st, launch, src, tgt, node_t, leaves, ptrs))
     partials = [None] * len(in_segs)
-    prev = None
-    carry_v = carry
-    devices = {id(w[1]) for w in work}
-    if len(devices) != 1:
-        raise TypeError("custom-operator scans across several GPUs are not supported; use add/multiply/"
-                        "minimum/maximum or place the vector on one device")
-    st = work[0][1]
-    st.ensure_results(2 * len(work) + 2)
     lib = _lib.load()
-    for j, (k, _st, launch, tgt) in enumerate(work):
+
+    def scan_one(j, st, launch, src, tgt, init_v, carry_v, carry_dev, slots):
+        if isinstance(src, ScanView):
+            run_scan_view(T, None, exclusive, src, tgt.ptr(), tgt.length, launch, combiner=op, init=init_v,
+                          carry_value=carry_v, carry_dev=carry_dev, seg_total_slot=slots[0],
+                          carry_out_slot=slots[1], scratch_index=j % 2)
+            return
         n = tgt.length
-        nbytes = int(lib.drk_jit_scan_scratch_bytes(n, tile))
-        scratch = st.scan_scratch(nbytes)
-        init_buf = _lib.scalar_buffer(init, T) if exclusive else None
-        carry_buf = _lib.scalar_buffer(carry_v, T) if (j == 0 and carry_v is not None) else None
+        scratch = st.scan_scratch(int(lib.drk_jit_scan_scratch_bytes(n, tile)), j % 2)
+        init_buf = _lib.scalar_buffer(init_v, T) if exclusive else None
+        carry_buf = _lib.scalar_buffer(carry_v, T) if carry_v is not None else None
         _lib.call("drk_jit_scan", mod.handle, b"drk_scan", T.itemsize, tile, tile * T.itemsize,
-                  1 if exclusive else 0, tgt.ptr(), tgt.ptr(), n,
+                  1 if exclusive else 0, src, tgt.ptr(), n,
                   ctypes.addressof(init_buf) if init_buf is not None else None,
-                  ctypes.addressof(carry_buf) if carry_buf is not None else None,
-                  st.result_dev_ptr(prev) if prev is not None else None,
-                  st.result_dev_ptr(2 * j), st.result_dev_ptr(2 * j + 1),
+                  ctypes.addressof(carry_buf) if carry_buf is not None else None, carry_dev,
+                  st.result_dev_ptr(slots[0]) if slots[0] is not None else None,
+                  st.result_dev_ptr(slots[1]) if slots[1] is not None else None,
                   scratch.data_ptr(), scratch.numel(), st.index, st.handle)
-        prev = 2 * j + 1
-    raw = st.fetch_results(2 * len(work))
-    for j, (k, *_r) in enumerate(work):
-        partials[k] = np.frombuffer(raw[16 * j: 16 * j + T.itemsize].tobytes(), dtype=T)[0].item()
+
+    from . import algorithms
+
+    if len({id(w[1]) for w in work}) == 1 and not algorithms._FORCE_MULTI_DEVICE_SCAN:
+        st = work[0][1]
+        st.ensure_results(2 * len(work) + 2)
+        prev = None
+        for j, (k, _st, launch, src, tgt, *_r) in enumerate(work):
+            scan_one(j, st, launch, src, tgt, init, carry if j == 0 else None,
+                     st.result_dev_ptr(prev) if prev is not None else None, (2 * j, 2 * j + 1))
+            prev = 2 * j + 1
+        raw = st.fetch_results(2 * len(work))
+        for j, (k, *_r) in enumerate(work):
+            partials[k] = np.frombuffer(raw[16 * j: 16 * j + T.itemsize].tobytes(), dtype=T)[0].item()
+        return partials
+    # several GPUs: totals on every GPU (in parallel), driver fold, carried scans
+    count = {}
+    for w in work:
+        count[id(w[1])] = count.get(id(w[1]), 0) + 1
+    for w in work:
+        w[1].ensure_results(count[id(w[1])])
+    slot_of, used = {}, {}
+    for k, st, launch, src, tgt, node_t, leaves, ptrs in work:
+        slot = used.get(id(st), 0)
+        used[id(st)] = slot + 1
+        slot_of[k] = slot
+        run_reduce(node_t, leaves, tgt.length, None, op, launch, slot, ptrs=ptrs)
+    fetched = {}
+    for w in work:
+        if id(w[1]) not in fetched:
+            fetched[id(w[1])] = w[1].fetch_host_results(count[id(w[1])])
+    for k, st, *_r in work:
+        raw = fetched[id(st)]
+        partials[k] = np.frombuffer(raw[8 * slot_of[k]: 8 * slot_of[k] + T.itemsize].tobytes(), dtype=T)[0].item()
+    prefix = carry
+    for j, (k, st, launch, src, tgt, *_r) in enumerate(work):
+        off = prefix
+        if partials[k] is not None:
+            prefix = partials[k] if prefix is None else op.fn(prefix, partials[k])
+        scan_one(j, st, launch, src, tgt, init, off, None, (None, None))
+    for w in work:
+        w[1].synchronize()
     return partials
+
+
+# ----------------------------------------------------------------------------------------
+# scan of a fused view (NVRTC loader for the L2 / single-pass scan templates)
+
+
+_SCAN_VIEW_PLANS = {}
+
+
+def scan_view_plan(view, T, opcode, combiner=None):
+    """(module, words, items) of the fused scan of `view` (kernels.ScanView: node already cast
+    to the output dtype T) with a libdrk operator or a traced custom combiner.  The module
+    defines drk_scan_l2_4 / drk_scan_l2_8 / drk_scan_1p over a generated loader whose
+    parameters are JitWords: one word per used leaf (pointer or index base), then constants
+    (kernel parameters, so expressions differing only in constants share one module)."""
+    T = np.dtype(T)
+    node, leaves = view.node, view.leaves
+    fk = expr._fn_key(combiner.fn) if combiner is not None else None
+    cacheable = combiner is None or fk is not None
+    used = sorted(expr.leaves_used(node))
+    key = (node.key(), _leaf_sig(leaves, used), T.str, opcode, fk)
+    plan = _SCAN_VIEW_PLANS.get(key) if cacheable else None
+    if plan is None:
+        plan = _scan_view_plan(node, leaves, T, opcode, combiner, used)
+        if cacheable:
+            if len(_SCAN_VIEW_PLANS) >= _PLAN_MAX:
+                _SCAN_VIEW_PLANS.clear()
+            _SCAN_VIEW_PLANS[key] = plan
+    mod, wvals, leaf_w, items = plan
+    words = list(wvals)
+    for k, w in leaf_w.items():
+        words[w] = view.ptrs[k] if leaves[k].kind != "index" else leaves[k].base
+    return mod, words, items
+
+
+def _scan_view_plan(node, leaves, T, opcode, combiner, used):
+    if opcode is None and combiner is not None:
+        code = match_binary(combiner.fn, T)
+        if code is not None:
+            opcode = code
+            combiner = None
+    opname, opsrc = _op_struct(opcode, combiner, T)
+    array_slots = [k for k in used if leaves[k].kind in ("array", "host")]
+    words = Words()
+    leaf_w = {k: words.add(0) for k in used}
+
+    def lv(k):
+        if leaves[k].kind == "index":
+            return f"(long long)(p.w[{leaf_w[k]}] + gi)"
+        return f"a{k}[e]"
+
+    def ls(k):
+        if leaves[k].kind == "index":
+            return f"(long long)(p.w[{leaf_w[k]}] + i)"
+        return f"(({ctype(leaves[k].dtype)}*)p.w[{leaf_w[k]}])[i]"
+
+    ev = Emitter(lv, words)
+    rv = ev.emit(node)
+    es = Emitter(ls, words)
+    es.consts = ev.consts
+    rs = es.emit(node)
+    if len(words.values) > _lib.JIT_WORDS:
+        raise JitError(f"fused scan needs {len(words.values)} parameter words (max {_lib.JIT_WORDS})")
+    V = ctype(T)
+    items = _scan_items(T)
+    loads = "\n".join(f"    {ctype(leaves[k].dtype)} a{k}[E];\n    drk::ldv_hint<{ctype(leaves[k].dtype)}, E>("
+                      f"(const {ctype(leaves[k].dtype)}*)p.w[{leaf_w[k]}] + i, a{k}, pol);" for k in array_slots)
+    nl = "\n      "
+    nl4 = "\n    "
+    params = f"drk::ScanParams<typename drk::WideAcc<{V}, {opname}>::type, drk::JitWords>"
+    src = f'''#include "drk_device.cuh"
+{opsrc}
+struct LD {{
+  typedef {V} V;
+  typedef drk::JitWords Params;
+  static constexpr bool bulk = false;
+  static constexpr int E = 16 / sizeof(V);
+  static __device__ __forceinline__ void load16(const Params& p, long long i, V (&v)[E], unsigned long long pol) {{
+{loads}
+#pragma unroll
+    for (int e = 0; e < E; ++e) {{
+      const long long gi = i + e;
+      (void)gi;
+      {nl.join(ev.lines)}
+      v[e] = (V)({rv});
+    }}
+  }}
+  static __device__ __forceinline__ V one(const Params& p, long long i) {{
+    {nl4.join(es.lines)}
+    return (V)({rs});
+  }}
+}};
+extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_l2_4(const {params} p) {{
+  drk::scan_l2_body<LD, {opname}, {BLOCK}, {items}, 4, 3>(p);
+}}
+extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_l2_8(const {params} p) {{
+  drk::scan_l2_body<LD, {opname}, {BLOCK}, {items}, 8, 3>(p);
+}}
+extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_1p(const {params} p) {{
+  drk::scan_kernel_body<LD, {V}, {opname}, {BLOCK}, {items}, 3>(p);
+}}
+'''
+    mod = compile_module(src, "drk_scan_view.cu")
+    return (mod, list(words.values), leaf_w, items)
 
 
 class _SegList:

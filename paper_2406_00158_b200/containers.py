@@ -84,15 +84,25 @@ class VectorSegment:
         return self.handle.span()[self.start : self.start + self.length]
 
     def eval_array(self):
-        """The segment as a device tensor (a view of its storage)."""
+        """The segment as a device tensor (a view of its storage).  In-flight asynchronous
+        transfers of the storage are ordered before any later work on its stream."""
+        rt = self.handle.runtime
+        if rt.backend == "cuda":
+            from .runtime import await_pending
+
+            await_pending(rt.state_of(self.handle.locale), [self.handle])
         return self.local_span()
 
     def store_array(self, values):
         """Overwrite the segment from a device tensor, host array or scalar."""
+        from .runtime import await_pending
+
         span = self.local_span()
         rt = self.handle.runtime
         rt._check_compute()
         st = rt.state_of(self.handle.locale)
+        # an upload still writing, or a download still reading, this storage lands first
+        await_pending(st, [self.handle])
         t = torch()
         with t.cuda.stream(st.stream):
             if isinstance(values, t.Tensor):

@@ -181,6 +181,15 @@ static int get_kernel(void* handle, const char* kernel, cudaKernel_t* k) {
 
 extern "C" int64_t drk_note_launch(void);
 
+// the kernel `kernel` of module `handle` as a function pointer for cudaLaunchKernelExC
+// (libdrk's own launchers of NVRTC scans, drk_jit_scan_view)
+extern "C" int drk_get_jit_kernel(void* handle, const char* kernel, const void** fn) {
+  cudaKernel_t k;
+  if (int rc = get_kernel(handle, kernel, &k)) return rc;
+  *fn = (const void*)k;
+  return 0;
+}
+
 extern "C" int drk_jit_launch(void* handle, const char* kernel, unsigned grid, unsigned block, unsigned smem,
                               const void* params, size_t params_bytes, int device, void* stream) {
   (void)params_bytes;

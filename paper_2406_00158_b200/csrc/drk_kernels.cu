@@ -148,8 +148,6 @@ static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
 static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
 static int g_scan_stagger = -1;  // ns between first-wave tile starts of the L2 scan (-1: automatic)
 static thread_local int g_chain_launch = 0;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
-static int g_scan_l2_pipe = 0;   // persistent two-tile pipeline (reduce next before look-back);
-                                 // measured slower than one 120 KB tile per CTA
 static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
 extern "C" int drk_scan_set_trace(void* buf) {
   g_scan_trace = buf;
@@ -184,9 +182,6 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_debug")) {
     old = g_scan_debug;
     g_scan_debug = value;
-  } else if (!strcmp(name, "scan_l2_pipe")) {
-    old = g_scan_l2_pipe;
-    g_scan_l2_pipe = value;
   } else if (!strcmp(name, "scan_l2_min")) {
     old = g_scan_l2_min;
     g_scan_l2_min = value;
@@ -788,81 +783,72 @@ static uint64_t next_epoch(void* scratch) {
   return ++g_scan_epochs[(uintptr_t)scratch];
 }
 
-template <class T, class Op, int SUBS, int ITEMS, int RING>
-static int launch_scan_l2dyn(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
-  constexpr int TILE = BLOCK * ITEMS * SUBS;
-  const int smem = RING * BLOCK * ITEMS * (int)sizeof(T);
-  const int64_t nt = (n + TILE - 1) / TILE;
-  auto p2 = p;
-  p2.ntiles = (u32)nt;
-  if (g_scan_l2_pipe) {
-    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, true, RING>;
-    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int64_t grid = (int64_t)sm_count(dev) * occupancy(k, BLOCK, smem);
-    if (grid > nt) grid = nt;
-    k<<<(unsigned)grid, BLOCK, smem, s>>>(p2);
-  } else {
-    auto k = scan_l2_kernel<T, Op, BLOCK, ITEMS, SUBS, false, RING>;
-    DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    // With more than two waves of tiles, every CTA lets a chained successor launch as soon as
-    // it starts (a no-op unless the next kernel is a DRK_SCAN_CHAINED scan): all of this grid
-    // has started only after most of it has finished, i.e. after its own wait for the scan
-    // before it, whose scratch the successor reuses.
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int64_t wave = (int64_t)sm_count(dev) * occupancy(k, BLOCK, smem);
-    p2.early_trigger = nt > 2 * wave;
-    // Stagger the first wave's reduces (ticket order) when the grid spans several waves:
-    // 2^26-2^28 elements gain 4-6 %; a single wave gains nothing (all tiles must be read
-    // before the last look-back resolves anyway)
-    p2.stagger_tiles = (u32)wave;
-    if (g_scan_stagger < 0) p2.stagger_ns = nt > 2 * wave ? 40 : 0;
-    if (g_chain_launch) {
-      // programmatic dependent of the previous scan of the chain (see carry_dev_read)
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)nt);
-      cfg.blockDim = dim3(BLOCK);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = s;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      attr[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      DRK_CHECK(cudaLaunchKernelEx(&cfg, k, p2));
-    } else {
-      k<<<(unsigned)nt, BLOCK, smem, s>>>(p2);
-    }
+// Launch an L2-scan kernel (AOT template instance or NVRTC kernel, given as a function
+// pointer) over ntiles tiles: stagger and early-trigger policy, and the programmatic-
+// dependent launch of a chained segment scan (drk_scan_ex DRK_SCAN_CHAINED).
+template <class A, class LP>
+static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int smem, int device, cudaStream_t s) {
+  const int64_t nt = (p.n + tile - 1) / tile;
+  if (nt > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
+  p.ntiles = (u32)nt;
+  DRK_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // With more than two waves of tiles, every CTA lets a chained successor launch as soon as
+  // it starts (a no-op unless the next kernel is a DRK_SCAN_CHAINED scan): all of this grid
+  // has started only after most of it has finished, i.e. after its own wait for the scan
+  // before it, whose scratch the successor reuses.
+  const int64_t wave = (int64_t)sm_count(device) * occupancy(fn, BLOCK, smem);
+  p.early_trigger = nt > 2 * wave;
+  // Stagger the first wave's reduces (ticket order) when the grid spans several waves:
+  // 2^26-2^28 elements gain 4-6 %; a single wave gains nothing (all tiles must be read
+  // before the last look-back resolves anyway)
+  p.stagger_tiles = (u32)wave;
+  if (g_scan_stagger < 0) p.stagger_ns = nt > 2 * wave ? 40 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nt);
+  cfg.blockDim = dim3(BLOCK);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (g_chain_launch) {
+    // programmatic dependent of the previous scan of the chain (see carry_dev_read)
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
   }
+  void* args[] = {&p};
+  DRK_CHECK(cudaLaunchKernelExC(&cfg, fn, args));
   return 0;
 }
 
-template <class T, class Op>
-static int launch_scan_l2_any(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+// 160 KB tiles (8 x 20 KB for 4-byte types); below 2^25 elements (about one wave of tiles)
+// 80 KB tiles, which give the grid more waves (2^23: 32.8 -> 26.9 us).  Other tile sizes
+// measured (3, 6, 7, 10, 12 sub-tiles) are not instantiated.
+static int l2_subs(int64_t n) { return g_scan_l2_subs == 4 || g_scan_l2_subs == 8 ? g_scan_l2_subs
+                                                                                   : (n < ((int64_t)1 << 25) ? 4 : 8); }
+
+template <class LDR, class Op>
+static int launch_scan_l2_any(ScanParams<typename WideAcc<typename LDR::V, Op>::type, typename LDR::Params>& p,
+                              int device, cudaStream_t s) {
+  typedef typename LDR::V T;
   constexpr int IT = ScanItems<T, Op>::value;
-  // 160 KB tiles (8 x 20 KB for 4-byte types); below 2^25 elements (about one wave of
-  // tiles) 80 KB tiles, which give the grid more waves (2^23: 32.8 -> 26.9 us)
-  const int subs = g_scan_l2_subs ? g_scan_l2_subs : (n < ((int64_t)1 << 25) ? 4 : 8);
+  const int subs = l2_subs(p.n);
   p.pre = g_scan_l2_pre;
-  switch (subs) {
-    // other tile sizes measured (3, 7, 10, 12 sub-tiles) are not instantiated; 6 stays for
-    // experiments
-    case 4: return launch_scan_l2dyn<T, Op, 4, IT, 3>(p, n, s);
-    case 6: return launch_scan_l2dyn<T, Op, 6, IT, 3>(p, n, s);
-    default: return launch_scan_l2dyn<T, Op, 8, IT, 3>(p, n, s);
-  }
+  const int smem = 3 * BLOCK * IT * (int)sizeof(T);
+  const void* fn = subs == 4 ? (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 4, 3>
+                             : (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 8, 3>;
+  return launch_l2_fn(fn, p, (int64_t)BLOCK * IT * subs, smem, device, s);
 }
 
 template <class T, class Op, int SUB>
-static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, cudaStream_t s) {
+static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, int device,
+                           cudaStream_t s) {
   constexpr int ITEMS = ScanItems<T, Op>::value;
   typedef ScanConfig<T, T, Op, BLOCK, ITEMS, SUB> C;
+  if (p.bulk_ok && g_scan_l2dyn && n >= (int64_t)g_scan_l2_min) return launch_scan_l2_any<PlainLoad<T>, Op>(p, device, s);
   const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
   if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
   p.ntiles = (u32)nt64;
-  if (p.bulk_ok && g_scan_l2dyn && n >= (int64_t)g_scan_l2_min) return launch_scan_l2_any<T, Op>(p, n, s);
   auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS, SUB>;
   if (C::SMEM > 48 * 1024) DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   k<<<p.ntiles, BLOCK, C::SMEM, s>>>(p);
@@ -900,7 +886,7 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   p.counter = (u32*)b;
   p.desc = (u64*)(b + 128);
   p.t0slot = (u64*)(b + 64);
-  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;  // < 0: automatic (launch_scan_l2dyn)
+  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;  // < 0: automatic (launch_l2_fn)
   p.epoch = next_epoch(scratch);
   p.bulk_ok = aligned16(in) && aligned16(out);
   p.trace = (u64*)g_scan_trace;
@@ -908,10 +894,10 @@ static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void
   cudaStream_t s = (cudaStream_t)stream;
   int rc = 0;
   switch (g_scan_sub) {
-    case 1: rc = launch_scan_sub<T, Op, 1>(p, n, s); break;
-    case 3: rc = launch_scan_sub<T, Op, 3>(p, n, s); break;
-    case 4: rc = launch_scan_sub<T, Op, 4>(p, n, s); break;
-    default: rc = launch_scan_sub<T, Op, 2>(p, n, s); break;
+    case 1: rc = launch_scan_sub<T, Op, 1>(p, n, device, s); break;
+    case 3: rc = launch_scan_sub<T, Op, 3>(p, n, device, s); break;
+    case 4: rc = launch_scan_sub<T, Op, 4>(p, n, device, s); break;
+    default: rc = launch_scan_sub<T, Op, 2>(p, n, device, s); break;
   }
   if (rc) return rc;
   return epilogue(what);
@@ -968,41 +954,22 @@ extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* 
 }
 
 // ---------------------------------------------------------------------------------------
-// batched segments: one L2-scan launch over the concatenation of up to DRK_SCAN_SEGS buffers
-// on one GPU (the segments of a vector that share a device), so the look-back carries the
-// prefix from segment to segment and there is one ramp-up and one tail instead of one per
-// segment.  Per-segment totals (the reference's partials, algorithms.py:234-274) are folded
-// afterwards from the per-tile aggregates, one warp per segment, in tile order.
+// batched segments: one L2-scan launch over up to DRK_SCAN_SEGS buffers on one GPU (the
+// segments of a vector that share a device), so there is one ramp-up and one tail instead of
+// one per segment.  Each segment's look-back stays inside the segment; its carry comes from
+// the last tile of the segment before it (segdesc), as the driver's fold of the rounded
+// partials (algorithms.py:234-274), and its total is written straight to seg_totals[k].
 
-template <class T, class Op>
-__global__ void __launch_bounds__(256) seg_totals_kernel(const u64* aggs,
-                                                         const ScanParams<typename WideAcc<T, Op>::type, const T*> p,
-                                                         char* out) {
-  typedef typename WideAcc<T, Op>::type A;
-  __shared__ Opt<A> s_warp[8];
-  const int k = blockIdx.x;
-  const u32 lo = p.seg_first[k], hi = p.seg_first[k + 1];
-  const u32 per = (hi - lo + 255) / 256;
-  const u32 a = lo + threadIdx.x * per;
-  Opt<A> acc;
-  acc.has = 0;
-  acc.v = A();
-  for (u32 t0 = a; t0 < a + per && t0 < hi; t0 += 8) {
-    u64 w[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) w[u] = (t0 + u < a + per && t0 + u < hi) ? __ldcg(aggs + t0 + u) : 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (t0 + u < a + per && t0 + u < hi) {
-        Opt<A> v;
-        v.has = 1;
-        v.v = from_bits<A>(w[u]);
-        acc = opt_combine<Op>(acc, v);
-      }
-    }
-  }
-  const Opt<A> tot = block_reduce<Op, A, 256>(acc, s_warp);  // thread order = tile order
-  if (threadIdx.x == 0) *(A*)(out + 8 * (size_t)k) = tot.v;
+static size_t batch_tiles(int dtype, int nseg, const int64_t* ns) {
+  const int64_t tile = (int64_t)BLOCK * 8 * ((dtype == DRK_F64 || dtype == DRK_I64) ? 10 : 20);
+  size_t nt = 0;
+  for (int k = 0; k < nseg; ++k) nt += (size_t)((ns[k] + tile - 1) / tile);
+  return nt;
+}
+
+extern "C" size_t drk_scan_batch_scratch_bytes(int dtype, int op, int nseg, const int64_t* ns) {
+  (void)op;
+  return 128 + batch_tiles(dtype, nseg, ns) * 16 + (DRK_SCAN_SEGS + 1) * 16;
 }
 
 template <class T, class Op>
@@ -1032,45 +999,35 @@ static int launch_scan_batch(int exclusive, int nseg, const void* const* ins, vo
   }
   p.seg_first[nseg] = (u32)nt;
   if (nt > 0x7fffffffull) return set_error(DRK_E_ARG, "drk_scan_batch: too many tiles");
-  const size_t need = 128 + nt * 16 + nt * 8;
+  const size_t need = 128 + nt * 16 + (DRK_SCAN_SEGS + 1) * 16;
   if (!scratch || scratch_bytes < need)
     return set_error(DRK_E_SCRATCH, "drk_scan_batch: scratch too small (need " + std::to_string(need) + ")");
   if (int rc = prologue(device, what)) return rc;
   char* b = (char*)scratch;
   p.nseg = nseg;
-  p.ntiles = (u32)nt;
+  p.n = (int64_t)nt * TILE;  // tile count for the launcher (segments carry their own lengths)
   p.exclusive = exclusive;
   p.has_init = init_host != nullptr;
   if (init_host) memcpy(&p.init, init_host, sizeof(A));
   p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
   if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
   p.carry_ptr = (const A*)carry_dev;
+  p.seg_total = (A*)seg_totals;
   p.carry_out = (A*)carry_out;
   p.counter = (u32*)b;
   p.desc = (u64*)(b + 128);
-  p.aggs = (u64*)(b + 128 + nt * 16);
+  p.segdesc = (u64*)(b + 128 + nt * 16);
+  p.t0slot = (u64*)(b + 64);
   p.epoch = next_epoch(scratch);
   p.bulk_ok = 1;
   p.pre = g_scan_l2_pre;
   p.debug = g_scan_debug;
+  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;
   const int smem = 3 * BLOCK * IT * (int)sizeof(T);
-  auto k = scan_l2_kernel<T, Op, BLOCK, IT, SUBS, false, 3>;
-  DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int64_t wave = (int64_t)sm_count(device) * occupancy(k, BLOCK, smem);
-  p.t0slot = (u64*)(b + 64);
-  p.stagger_tiles = (u32)wave;
-  p.stagger_ns = g_scan_stagger >= 0 ? (u32)g_scan_stagger : ((int64_t)nt > 2 * wave ? 40u : 0u);
-  k<<<(unsigned)nt, BLOCK, smem, (cudaStream_t)stream>>>(p);
-  if (seg_totals) seg_totals_kernel<T, Op><<<nseg, 256, 0, (cudaStream_t)stream>>>(p.aggs, p, (char*)seg_totals);
+  if (int rc = launch_l2_fn((const void*)scan_l2_kernel<PlainLoad<T>, Op, BLOCK, IT, SUBS, 3>, p, TILE, smem, device,
+                            (cudaStream_t)stream))
+    return rc;
   return epilogue(what);
-}
-
-extern "C" size_t drk_scan_batch_scratch_bytes(int dtype, int op, int nseg, const int64_t* ns) {
-  (void)op;
-  const int64_t tile = (int64_t)BLOCK * 8 * ((dtype == DRK_F64 || dtype == DRK_I64) ? 10 : 20);
-  size_t nt = 0;
-  for (int k = 0; k < nseg; ++k) nt += (size_t)((ns[k] + tile - 1) / tile);
-  return 128 + nt * 24;
 }
 
 template <class T>
@@ -1117,6 +1074,168 @@ extern "C" int drk_scan_ex(int dtype, int op, int exclusive, int flags, const vo
                           carry_out_dev, scratch, scratch_bytes, device, stream);
   g_chain_launch = 0;
   return rc;
+}
+
+// ---------------------------------------------------------------------------------------
+// scans of fused views: inclusive_scan(transform(x, f), out) reads the leaves of the view and
+// writes only `out` (reference views.py:164-181 materialises f(x) first, algorithms.py:198-202
+// then scans it).  The loader (AOT ProdScanLoad / AffineScanLoad, or NVRTC-generated) gets
+// its leaf pointers and constants as JitWords.
+
+template <class A>
+static int fill_view_params(ScanParams<A, JitWords>& p, const uint64_t* words, int nwords, void* out, int64_t n,
+                            int exclusive, const void* init_host, const void* carry_host, const void* carry_dev,
+                            void* seg_total, void* carry_out, void* scratch, size_t scratch_bytes, size_t need,
+                            const char* what) {
+  if (n < 1) return set_error(DRK_E_ARG, std::string(what) + ": n must be >= 1");
+  if (!out || !words) return set_error(DRK_E_ARG, std::string(what) + ": null out/words");
+  if (nwords < 0 || nwords > DRK_JIT_WORDS)
+    return set_error(DRK_E_ARG, std::string(what) + ": at most " + std::to_string(DRK_JIT_WORDS) + " words");
+  if (exclusive && !init_host) return set_error(DRK_E_ARG, std::string(what) + ": exclusive scan needs init");
+  if (carry_host && carry_dev) return set_error(DRK_E_ARG, std::string(what) + ": give at most one carry");
+  if (!scratch || scratch_bytes < need)
+    return set_error(DRK_E_SCRATCH, std::string(what) + ": scratch too small (need " + std::to_string(need) + ")");
+  memset(&p, 0, sizeof(p));
+  memcpy(p.in.w, words, sizeof(uint64_t) * nwords);
+  p.out = out;
+  p.n = n;
+  p.exclusive = exclusive;
+  p.has_init = init_host != nullptr;
+  if (init_host) memcpy(&p.init, init_host, sizeof(A));
+  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
+  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
+  p.carry_ptr = (const A*)carry_dev;
+  p.seg_total = (A*)seg_total;
+  p.carry_out = (A*)carry_out;
+  char* b = (char*)scratch;
+  p.counter = (u32*)b;
+  p.t0slot = (u64*)(b + 64);
+  p.desc = (u64*)(b + 128);
+  p.epoch = next_epoch(scratch);
+  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;
+  p.trace = (u64*)g_scan_trace;
+  p.debug = g_scan_debug;
+  return 0;
+}
+
+// One fused-view scan: the L2 kernel (l2_4 / l2_8 by size) when every leaf is vector-aligned
+// (vec_ok) and out is 16-byte aligned, else the single-pass kernel `one` (3 sub-tiles).
+template <class A>
+static int launch_view_scan(const void* l2_4, const void* l2_8, const void* one, int v_bytes,
+                            ScanParams<A, JitWords>& p, int vec_ok, int device, cudaStream_t s) {
+  const int items = v_bytes == 4 ? 20 : 10;
+  if (vec_ok && aligned16(p.out) && g_scan_l2dyn && p.n >= (int64_t)g_scan_l2_min) {
+    p.bulk_ok = 1;
+    p.pre = g_scan_l2_pre;
+    const int subs = l2_subs(p.n);
+    return launch_l2_fn(subs == 4 ? l2_4 : l2_8, p, (int64_t)BLOCK * items * subs, 3 * BLOCK * items * v_bytes, device,
+                        s);
+  }
+  constexpr int SUB = 3;
+  const int64_t tile = (int64_t)BLOCK * items * SUB;
+  const int64_t nt = (p.n + tile - 1) / tile;
+  if (nt > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan_view: too many tiles");
+  p.ntiles = (u32)nt;
+  p.bulk_ok = 0;
+  const int smem = (int)tile * v_bytes;
+  DRK_CHECK(cudaFuncSetAttribute(one, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nt);
+  cfg.blockDim = dim3(BLOCK);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  void* args[] = {&p};
+  DRK_CHECK(cudaLaunchKernelExC(&cfg, one, args));
+  return 0;
+}
+
+template <class LDR, class Op>
+static int view_scan_aot(const uint64_t* words, int nwords, int vec_ok, int exclusive, void* out, int64_t n,
+                         const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total,
+                         void* carry_out, void* scratch, size_t scratch_bytes, int device, void* stream) {
+  typedef typename LDR::V T;
+  typedef typename WideAcc<T, Op>::type A;
+  constexpr int IT = ScanItems<T, Op>::value;
+  const char* what = "drk_scan_view";
+  ScanParams<A, JitWords> p;
+  if (int rc = fill_view_params(p, words, nwords, out, n, exclusive, init_host, carry_host, carry_dev, seg_total,
+                                carry_out, scratch, scratch_bytes, scan_scratch<T, Op>(n), what))
+    return rc;
+  if (int rc = prologue(device, what)) return rc;
+  if (int rc = launch_view_scan(
+          (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 4, 3>, (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 8, 3>,
+          (const void*)scan_kernel<LDR, T, Op, BLOCK, IT, 3>, (int)sizeof(T), p, vec_ok, device, (cudaStream_t)stream))
+    return rc;
+  return epilogue(what);
+}
+
+extern "C" int drk_scan_view(int kind, int dtype, int op, int exclusive, const uint64_t* words, int nwords,
+                             int vec_ok, void* out, int64_t n, const void* init_host, const void* carry_host,
+                             const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
+                             size_t scratch_bytes, int device, void* stream) {
+  if (op != DRK_ADD) return set_error(DRK_E_ARG, "drk_scan_view: the AOT view scans take op = DRK_ADD");
+  if (kind != DRK_VIEW_PRODUCT && kind != DRK_VIEW_AFFINE) return set_error(DRK_E_ARG, "drk_scan_view: unknown kind");
+  DRK_DISPATCH(dtype, "drk_scan_view", T, {
+    if (kind == DRK_VIEW_PRODUCT)
+      return view_scan_aot<ProdScanLoad<T>, OpAdd>(words, nwords, vec_ok, exclusive, out, n, init_host, carry_host,
+                                                    carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes,
+                                                    device, stream);
+    return view_scan_aot<AffineScanLoad<T>, OpAdd>(words, nwords, vec_ok, exclusive, out, n, init_host, carry_host,
+                                                    carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes,
+                                                    device, stream);
+  });
+}
+
+extern "C" int drk_scan_view_ex(int kind, int dtype, int op, int exclusive, int flags, const uint64_t* words,
+                                int nwords, int vec_ok, void* out, int64_t n, const void* init_host,
+                                const void* carry_host, const void* carry_dev, void* seg_total_dev,
+                                void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream) {
+  if (flags & ~DRK_SCAN_CHAINED) return set_error(DRK_E_ARG, "drk_scan_view_ex: unknown flags");
+  if ((flags & DRK_SCAN_CHAINED) && !carry_dev)
+    return set_error(DRK_E_ARG, "drk_scan_view_ex: a chained scan takes its carry from the previous scan");
+  g_chain_launch = (flags & DRK_SCAN_CHAINED) != 0;
+  const int rc = drk_scan_view(kind, dtype, op, exclusive, words, nwords, vec_ok, out, n, init_host, carry_host,
+                               carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes, device, stream);
+  g_chain_launch = 0;
+  return rc;
+}
+
+// NVRTC view scans: the module defines drk_scan_l2_4 / drk_scan_l2_8 (scan_l2_body) and
+// drk_scan_1p (scan_kernel_body, 3 sub-tiles) over its generated loader.
+extern "C" int drk_get_jit_kernel(void* handle, const char* kernel, const void** fn);
+
+extern "C" int drk_jit_scan_view(void* handle, int v_bytes, int acc_bytes, int exclusive, int flags,
+                                 const uint64_t* words, int nwords, int vec_ok, void* out, int64_t n,
+                                 const void* init_host, const void* carry_host, const void* carry_dev,
+                                 void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
+                                 int device, void* stream) {
+  const char* what = "drk_jit_scan_view";
+  if (v_bytes != 4 && v_bytes != 8) return set_error(DRK_E_ARG, "drk_jit_scan_view: v_bytes must be 4 or 8");
+  if (flags & ~DRK_SCAN_CHAINED) return set_error(DRK_E_ARG, "drk_jit_scan_view: unknown flags");
+  const void *k4 = nullptr, *k8 = nullptr, *k1 = nullptr;
+  if (int rc = drk_get_jit_kernel(handle, "drk_scan_l2_4", &k4)) return set_error(rc, "drk_jit_scan_view: no kernel");
+  if (int rc = drk_get_jit_kernel(handle, "drk_scan_l2_8", &k8)) return set_error(rc, "drk_jit_scan_view: no kernel");
+  if (int rc = drk_get_jit_kernel(handle, "drk_scan_1p", &k1)) return set_error(rc, "drk_jit_scan_view: no kernel");
+  const size_t need = 128 + (size_t)((n + BLOCK * (v_bytes == 4 ? 20 : 10) - 1) / (BLOCK * (v_bytes == 4 ? 20 : 10))) * 16;
+  if (int rc = prologue(device, what)) return rc;
+  g_chain_launch = (flags & DRK_SCAN_CHAINED) != 0;
+  int rc = 0;
+  if (acc_bytes == 8) {
+    ScanParams<double, JitWords> p;
+    rc = fill_view_params(p, words, nwords, out, n, exclusive, init_host, carry_host, carry_dev, seg_total_dev,
+                          carry_out_dev, scratch, scratch_bytes, need, what);
+    if (!rc) rc = launch_view_scan(k4, k8, k1, v_bytes, p, vec_ok, device, (cudaStream_t)stream);
+  } else if (acc_bytes == 4) {
+    ScanParams<float, JitWords> p;
+    rc = fill_view_params(p, words, nwords, out, n, exclusive, init_host, carry_host, carry_dev, seg_total_dev,
+                          carry_out_dev, scratch, scratch_bytes, need, what);
+    if (!rc) rc = launch_view_scan(k4, k8, k1, v_bytes, p, vec_ok, device, (cudaStream_t)stream);
+  } else {
+    rc = set_error(DRK_E_ARG, "drk_jit_scan_view: acc_bytes must be 4 or 8");
+  }
+  g_chain_launch = 0;
+  if (rc) return rc;
+  return epilogue(what);
 }
 
 // ---------------------------------------------------------------------------------------

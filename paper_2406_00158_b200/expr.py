@@ -472,27 +472,96 @@ _TRACES = {}
 _TRACE_CACHE_MAX = 4096
 
 
-def _fn_key(fn):
-    """A hashable identity of a function's behaviour: code, defaults, closure contents and
-    the referenced globals.  None if any of those is unhashable (no caching then)."""
+class _Uncacheable(Exception):
+    pass
+
+
+# modules whose attributes a traced function may read without defeating the cache: their
+# contents are functions/ufuncs/constants, not user state
+_STABLE_MODULES = ("numpy", "math", "operator", "scipy", "cmath", "builtins")
+
+
+def _freeze(v, depth):
+    """A hashable, type-exact snapshot of a value a traced function can see, or
+    _Uncacheable.  Keyed by type and exact value: 2 and 2.0, 0.0 and -0.0, np.float64(0.5)
+    and 0.5 all differ (their traces differ under numpy's promotion rules)."""
+    import types
+
+    if v is None or isinstance(v, (bool, str, bytes)):
+        return (type(v), v)
+    if isinstance(v, (int, float, complex)) and not isinstance(v, np.generic):
+        return (type(v), repr(v))  # repr separates -0.0 from 0.0 and keeps the type exact
+    if isinstance(v, np.generic):
+        return (type(v), v.dtype.str, v.tobytes())
+    if isinstance(v, np.dtype):
+        return ("dtype", v.str)
+    if isinstance(v, type):
+        return ("type", v)  # classes (np.float32, int ...) are used as dtypes/constructors
+    if isinstance(v, (tuple, frozenset)):
+        return (type(v), tuple(_freeze(x, depth) for x in v))
+    if isinstance(v, np.ufunc) or v is _ERF:
+        return ("ufunc", v)
+    if isinstance(v, types.BuiltinFunctionType):
+        return ("builtin", v)
+    if isinstance(v, types.ModuleType):
+        if v.__name__.split(".")[0] in _STABLE_MODULES:
+            return ("module", v.__name__)
+        raise _Uncacheable(v.__name__)
+    if isinstance(v, DeviceFunction):
+        return ("devfn", id(v), v.name)
+    if isinstance(v, types.FunctionType):
+        if depth > 4:
+            raise _Uncacheable("helper nesting")
+        return ("fn", _fn_key_strict(v, depth + 1))
+    if isinstance(v, functools_partial()):
+        return ("partial", _freeze(v.func, depth + 1), _freeze(tuple(v.args), depth),
+                _freeze(tuple(sorted((v.keywords or {}).items())), depth))
+    # objects with mutable state (instances, lists, dicts, arrays, modules of user code):
+    # the function may read anything through them, so its trace is not cached
+    raise _Uncacheable(type(v).__name__)
+
+
+def functools_partial():
+    import functools
+
+    return functools.partial
+
+
+def _fn_key_strict(fn, depth=0):
     code = getattr(fn, "__code__", None)
     if code is None:
-        return None
+        raise _Uncacheable("no code")
+    cells = tuple(_freeze(c.cell_contents, depth) for c in (fn.__closure__ or ()))
+    g = fn.__globals__
+    glob = tuple((nm, _freeze(g[nm], depth)) for nm in code.co_names if nm in g)
+    defaults = _freeze(tuple(fn.__defaults__ or ()), depth)
+    kwdefaults = _freeze(tuple(sorted((fn.__kwdefaults__ or {}).items())), depth)
+    return (code, defaults, kwdefaults, cells, glob)
+
+
+def _fn_key(fn):
+    """A hashable identity of a function's behaviour: its code, defaults, closure contents
+    and the globals it names, each frozen by type and exact value (helper functions
+    recursively).  None — no caching, the function is traced on every call like the
+    reference calls it every time — when it can reach mutable state (an object attribute,
+    a list, an array, a user module) whose value could change between calls."""
+    if isinstance(fn, functools_partial()):
+        try:
+            return ("partial", _freeze(fn, 0))
+        except (_Uncacheable, TypeError, ValueError):
+            return None
     try:
-        cells = tuple(c.cell_contents for c in (fn.__closure__ or ()))
-        g = fn.__globals__
-        glob = tuple((nm, g[nm]) for nm in code.co_names if nm in g and not callable(g[nm])
-                     and not hasattr(g[nm], "__dict__"))
-        key = (code, fn.__defaults__, cells, glob)
+        key = _fn_key_strict(fn)
         hash(key)
         return key
-    except Exception:
+    except (_Uncacheable, TypeError, ValueError):
         return None
 
 
-def trace_cached(fn, value, value_key):
+def trace_cached(fn, value, value_key, fk=None):
     """trace() memoised on (function identity, lowered value structure)."""
-    fk = _fn_key(fn)
+    if fk is None:
+        fk = _fn_key(fn)
     if fk is None:
         return trace(fn, value)
     key = (fk, value_key)

@@ -287,12 +287,15 @@ def catalogue_reduce(node, leaves, opcode, device):
     return None
 
 
-def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
+def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int, *, ptrs=None, result_ptr=None):
     """Reduce `node` over n elements into host result slot `slot` of launch.state (value in
-    drk_acc_dtype(node.dtype, op) for catalogue ops; read with fetch_host_results)."""
-    ptrs = stage_leaves(leaves, launch)
+    drk_acc_dtype(node.dtype, op) for catalogue ops; read with fetch_host_results), or into
+    the device address result_ptr.  ptrs: the leaves' pointers if already staged."""
+    if ptrs is None:
+        ptrs = stage_leaves(leaves, launch)
     st = launch.state
-    res = st.host_result_dev_ptr(slot)  # stored straight into mapped pinned memory
+    # stored straight into mapped pinned memory unless a device slot is given
+    res = result_ptr if result_ptr is not None else st.host_result_dev_ptr(slot)
     T = node.dtype
     if opcode is not None and T in _lib.DTYPE_CODE:
         code = _lib.DTYPE_CODE[T]
@@ -308,7 +311,7 @@ def run_reduce(node, leaves, n, opcode, combiner, launch: Launch, slot: int):
             return
     from . import codegen
 
-    codegen.run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot)
+    codegen.run_reduce(node, leaves, ptrs, n, opcode, combiner, launch, slot, result_ptr=result_ptr)
 
 
 # ----------------------------------------------------------------------------------------
@@ -329,10 +332,7 @@ def run_scan(dtype, opcode, exclusive, in_ptr, out_ptr, n, lctx: Launch, *, init
     code = _lib.dtype_code(T)
     A = _lib.acc_dtype(T, opcode)
     st = lctx.state
-    key = (code, opcode, n)
-    nbytes = _SCAN_SCRATCH_BYTES.get(key)
-    if nbytes is None:
-        nbytes = _SCAN_SCRATCH_BYTES[key] = int(_lib.load().drk_scan_scratch_bytes(code, opcode, n))
+    nbytes = _scan_scratch_bytes(code, opcode, n)
     scratch = st.scan_scratch(nbytes, scratch_index)
     init_buf = _keep(lctx, _scalar_arg(init, A)) if init is not None else None
     carry_buf = _keep(lctx, _scalar_arg(carry_value, A)) if carry_value is not None else None
@@ -346,3 +346,126 @@ def run_scan(dtype, opcode, exclusive, in_ptr, out_ptr, n, lctx: Launch, *, init
         st.result_dev_ptr(carry_out_slot) if carry_out_slot is not None else None,
         scratch.data_ptr(), scratch.numel(),
     )
+
+
+# ----------------------------------------------------------------------------------------
+# scan of a fused view
+
+
+class ScanView:
+    """What a fused segment scan reads: `node` (already cast to the output dtype) over
+    `leaves`, whose device pointers are `ptrs` (kernels.stage_leaves)."""
+
+    __slots__ = ("node", "leaves", "ptrs", "n")
+
+    def __init__(self, node, leaves, ptrs, n):
+        self.node = node
+        self.leaves = leaves
+        self.ptrs = ptrs
+        self.n = n
+
+    def vec_ok(self) -> bool:
+        return all(self.ptrs[k] % 16 == 0 for k in _array_slots(self.node, self.leaves))
+
+
+def _array_slots(node, leaves):
+    from . import expr
+
+    return sorted(k for k in expr.leaves_used(node) if leaves[k].kind in ("array", "host"))
+
+
+def match_scan_view(node, leaves, opcode, T):
+    """AOT fused-scan loader for `node` (dtype T) with add: (kind, words) or None.
+    PRODUCT x*y (zip|transform dot shape); AFFINE alpha*x, alpha*x + beta, x + beta, x - beta
+    — exactly numpy's roundings (one per operation, no FMA)."""
+    T = np.dtype(T)
+    if opcode != _lib.ADD or T not in _lib.DTYPE_CODE or node.dtype != T or not _uniform(node, T):
+        return None
+    from .codegen import const_bits
+
+    if node.op == "multiply":
+        a, b = node.args
+        if _is_leaf(a, leaves) and _is_leaf(b, leaves):
+            return _lib.VIEW_PRODUCT, ("leaf", a.value), ("leaf", b.value)
+        if b.op == "const" and _is_leaf(a, leaves):
+            a, b = b, a
+        if a.op == "const" and _is_leaf(b, leaves):
+            return _lib.VIEW_AFFINE, ("leaf", b.value), const_bits(a.value, T), 0, 0
+        return None
+    if node.op in ("add", "subtract"):
+        x, c = node.args
+        if node.op == "add" and x.op == "const":
+            x, c = c, x
+        if c.op != "const":
+            return None
+        beta = c.value if node.op == "add" else -np.asarray(c.value, dtype=T)
+        if _is_leaf(x, leaves):
+            return _lib.VIEW_AFFINE, ("leaf", x.value), const_bits(1, T), const_bits(beta, T), 1
+        if x.op == "multiply" and _uniform(x, T):
+            p, q = x.args
+            if q.op == "const" and _is_leaf(p, leaves):
+                p, q = q, p
+            if p.op == "const" and _is_leaf(q, leaves):
+                return _lib.VIEW_AFFINE, ("leaf", q.value), const_bits(p.value, T), const_bits(beta, T), 1
+    return None
+
+
+def run_scan_view(T, opcode, exclusive, view: ScanView, out_ptr, n, lctx: Launch, *, combiner=None, init=None,
+                  carry_value=None, carry_dev=None, seg_total_slot=None, carry_out_slot=None, chained=False,
+                  scratch_index=0):
+    """One fused scan of a view segment: out = scan(view) with the view's values computed from
+    its leaves inside the scan kernel (AOT drk_scan_view for product / affine views with add,
+    an NVRTC module otherwise) — no intermediate array."""
+    T = np.dtype(T)
+    st = lctx.state
+    A = _lib.acc_dtype(T, opcode) if opcode is not None else T
+    init_buf = _keep(lctx, _scalar_arg(init, A)) if init is not None else None
+    carry_buf = _keep(lctx, _scalar_arg(carry_value, A)) if carry_value is not None else None
+    tail = (
+        1 if exclusive else 0,
+    )
+    common = (out_ptr, n,
+              ctypes.addressof(init_buf) if init_buf is not None else None,
+              ctypes.addressof(carry_buf) if carry_buf is not None else None,
+              carry_dev,
+              st.result_dev_ptr(seg_total_slot) if seg_total_slot is not None else None,
+              st.result_dev_ptr(carry_out_slot) if carry_out_slot is not None else None)
+    flags = _lib.SCAN_CHAINED if chained else 0
+    m = match_scan_view(view.node, view.leaves, opcode, T) if combiner is None else None
+    if m is not None:
+        kind, *parts = m
+        words = [view.ptrs[x[1]] if isinstance(x, tuple) else x for x in parts]
+        wbuf = _keep(lctx, (ctypes.c_uint64 * len(words))(*[w & 0xFFFFFFFFFFFFFFFF for w in words]))
+        code = _lib.dtype_code(T)
+        nbytes = _scan_scratch_bytes(code, opcode, n)
+        scratch = st.scan_scratch(nbytes, scratch_index)
+        launch_kernel("drk_scan_view_ex", lctx, n, kind, code, opcode, *tail, flags, wbuf, len(words),
+                      1 if view.vec_ok() else 0, *common, scratch.data_ptr(), scratch.numel())
+        return
+    from . import codegen
+
+    mod, words, items = codegen.scan_view_plan(view, T, opcode, combiner)
+    wbuf = _keep(lctx, (ctypes.c_uint64 * len(words))(*[w & 0xFFFFFFFFFFFFFFFF for w in words]))
+    nbytes = int(_lib.load().drk_jit_scan_scratch_bytes(n, 256 * items))
+    scratch = st.scan_scratch(nbytes, scratch_index)
+    args = (mod.handle, T.itemsize, A.itemsize, *tail, flags, wbuf, len(words), 1 if view.vec_ok() else 0, *common,
+            scratch.data_ptr(), scratch.numel(), st.index, st.handle)
+    if _PROFILE is None:
+        _lib.call("drk_jit_scan_view", *args)
+        return
+    from .runtime import torch
+
+    t = torch()
+    s_, e_ = t.cuda.Event(enable_timing=True), t.cuda.Event(enable_timing=True)
+    s_.record(st.stream)
+    _lib.call("drk_jit_scan_view", *args)
+    e_.record(st.stream)
+    _PROFILE.setdefault("drk_scan", []).append((s_, e_, n))
+
+
+def _scan_scratch_bytes(code, opcode, n):
+    key = (code, opcode, n)
+    nbytes = _SCAN_SCRATCH_BYTES.get(key)
+    if nbytes is None:
+        nbytes = _SCAN_SCRATCH_BYTES[key] = int(_lib.load().drk_scan_scratch_bytes(code, opcode, n))
+    return nbytes

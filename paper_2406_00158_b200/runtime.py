@@ -498,6 +498,10 @@ class Runtime:
             d[...] = s  # host to host
             return TaskTicket(None, None, ())
         self._check_compute()
+        # asynchronous uploads still writing either side, or downloads still reading the
+        # destination, complete before this copy reads or overwrites them
+        # (every branch below enqueues the copy on st's stream, or syncs it first)
+        await_pending(st, [h for h in (src, dst) if isinstance(h, StorageHandle)])
         t = torch()
         s_t = t.from_numpy(np.ascontiguousarray(s)) if isinstance(s, np.ndarray) else s
         if isinstance(d, np.ndarray):

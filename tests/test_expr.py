@@ -133,3 +133,112 @@ def test_match_binary():
     assert codegen.match_binary(lambda a, b: b * a, np.dtype(np.float64)) == 1
     assert codegen.match_binary(lambda a, b: np.minimum(a, b), np.dtype(np.float64)) == 2
     assert codegen.match_binary(lambda a, b: a + b + 1, np.dtype(np.int64)) is None
+
+
+# ----------------------------------------------------------------------------------------
+# trace cache: a cached trace must never outlive the state it was traced from
+
+
+class _Params:
+    alpha = 2.0
+
+
+def _consts(node):
+    return sorted((n.value, n.dtype.str) for n in node.walk() if n.op == "const")
+
+
+def test_trace_cache_sees_attribute_mutation(meta_rt):
+    p = _Params()
+    x = sr.DistributedVector(meta_rt[2], 10, dtype=np.float64)
+    v = views.transform(x, lambda t: t * p.alpha)
+    seg = v.segments()[0]
+    assert _consts(views.lower(seg).value) == [(2.0, "<f8")]
+    p.alpha = 3.0
+    assert _consts(views.lower(v.segments()[0]).value) == [(3.0, "<f8")]
+    assert expr._fn_key(lambda t: t * p.alpha) is None  # reaches an object attribute
+
+
+def test_trace_cache_keys_closure_by_type_and_value():
+    leaf = expr.leaf(0, np.int32)
+    out = []
+    for a in (2, 2.0, np.float64(2.0), 0.0, -0.0):
+        fn = (lambda a_: (lambda t: t * a_))(a)
+        node = expr.trace_cached(fn, leaf, ("k",))
+        out.append((node.dtype.str, _consts(node)))
+    assert out[0][0] == "<i4"          # int32 * 2 stays int32
+    assert out[1][0] == "<f8"          # int32 * 2.0 -> float64 (NEP 50), not the cached int32 trace
+    assert out[2][0] == "<f8"
+    assert out[3][1] != out[4][1] or repr(out[3][1]) != repr(out[4][1])
+
+
+def test_trace_cache_follows_globals_and_helpers():
+    g = {"np": np, "K": 2}
+    exec("def helper(t):\n    return t * K\n\ndef f(t):\n    return helper(t) + 1\n", g)
+    leaf = expr.leaf(0, np.float64)
+    a = expr.trace_cached(g["f"], leaf, ("g",))
+    g["K"] = 5
+    b = expr.trace_cached(g["f"], leaf, ("g",))
+    assert (5, "<f8") not in [(c[0], c[1]) for c in _consts(a)]
+    assert any(c[0] == 5 for c in _consts(b))
+    g["state"] = [1]
+    exec("def h(t):\n    return t * state[0]\n", g)
+    assert expr._fn_key(g["h"]) is None  # a list can change under the cache
+
+
+def test_trace_cache_keys_stay_hashable_for_numpy_functions():
+    fn = lambda t: np.sqrt(t) * np.float32(1.5)  # noqa: E731
+    assert expr._fn_key(fn) is not None
+
+
+# ----------------------------------------------------------------------------------------
+# fused view scans (compile only; the GPU parity tests run them)
+
+
+def _scan_view_source(monkeypatch, node, leaves, T, opcode, combiner=None):
+    got = {}
+
+    def fake_compile(src, name):
+        got["src"] = src
+        return codegen.Module(None)
+
+    monkeypatch.setattr(codegen, "compile_module", fake_compile)
+    codegen._SCAN_VIEW_PLANS.clear()
+    view = kernels.ScanView(node, leaves, [0] * len(leaves), 100)
+    mod, words, items = codegen.scan_view_plan(view, T, opcode, combiner)
+    return got["src"], words, items
+
+
+@pytest.mark.parametrize("T", [np.float32, np.int64])
+def test_scan_view_nvrtc_compiles(meta_rt, monkeypatch, T):
+    lw = _lowered(meta_rt, [T, np.float64])
+    node = expr.cast(expr.trace(lambda t: np.sqrt(t[0] * t[1] + 1.5) * 2, lw.value), T)
+    src, words, items = _scan_view_source(monkeypatch, node, lw.leaves, np.dtype(T), 0)
+    assert "drk_scan_l2_8" in src and "drk_scan_1p" in src
+    assert len(words) <= 16 and items == (20 if np.dtype(T).itemsize == 4 else 10)
+    assert len(codegen.cubin_for(src, "scan_view.cu")) > 1000
+
+
+def test_scan_view_custom_combiner_compiles(meta_rt, monkeypatch):
+    lw = _lowered(meta_rt, [np.float64, np.float64])
+    node = expr.trace(lambda t: t[0] * 0.5, lw.value)
+    op = sr.BinaryOp(lambda a, b: np.maximum(a, b) + 0.25 * b)
+    src, words, _ = _scan_view_source(monkeypatch, node, lw.leaves, np.dtype(np.float64), None, op)
+    assert "OpC" in src
+    assert len(codegen.cubin_for(src, "scan_view.cu")) > 1000
+
+
+def test_scan_view_catalogue(meta_rt):
+    lw = _lowered(meta_rt, [np.float32, np.float32])
+    f32 = np.dtype(np.float32)
+    prod = expr.trace(lambda t: t[0] * t[1], lw.value)
+    assert kernels.match_scan_view(prod, lw.leaves, 0, f32)[0] == 1
+    aff = expr.trace(lambda t: 2.5 * t[0] + 1.0, lw.value)
+    m = kernels.match_scan_view(aff, lw.leaves, 0, f32)
+    assert m[0] == 2 and m[1] == ("leaf", 0) and m[4] == 1
+    sub = expr.trace(lambda t: t[1] - 3.0, lw.value)
+    m = kernels.match_scan_view(sub, lw.leaves, 0, f32)
+    assert m[0] == 2 and codegen.const_bits(-3.0, f32) == m[3]
+    assert kernels.match_scan_view(prod, lw.leaves, 1, f32) is None  # multiply-scan: NVRTC
+    li = _lowered(meta_rt, [np.int32, np.int32])
+    mixed = expr.trace(lambda t: t[0] * 2.5, li.value)  # int32 * 2.5 -> float64
+    assert kernels.match_scan_view(mixed, li.leaves, 0, f32) is None
