@@ -4,16 +4,24 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one process per GPU, NCCL)
 
-Workload (BASELINE.json north star, configs[1]/[2]): fp32 distributed vectors of 2^30
-elements PER GPU (weak scaling).  One step = the three headline pipelines through the
-public API, exactly as a user writes them:
+Two multi-GPU modes, both with weak scaling (2^log2n elements PER GPU):
+  * shp (no torchrun): the paper's single-process multi-GPU runtime — one Runtime over N
+    GPUs, a distributed vector of N * 2^log2n elements with one segment per GPU (or
+    --segments S per GPU).  reduce folds the per-GPU partials on the driver (or with NCCL,
+    --combine nccl), scan runs the two-pass schedule with the carry folded on the devices
+    from peer memory.  Timing: CUDA events on every GPU's stream, max over GPUs.
+    DRK_BENCH_SHARE_GPU=1 (or --share-gpu) puts all N GPUs' segments on GPU 0 — a test
+    mode for one-GPU hosts whose timings are not measurements.
+  * spmd (torchrun): one process per GPU, each holding its block of the vector; the
+    reduce / scan combine steps are NCCL collectives (spmd.py).  Max over ranks.
+
+One step = the three headline pipelines through the public API, as a user writes them:
     dot    = reduce(transform(zip(b, c), t0*t1))          8 B/elem   (bench.dot_product)
     triad  = for_each(zip(a, b, c), (t1 + 3*t2, -, -))    12 B/elem  (bench.stream_triad)
     scan   = inclusive_scan(c, a)                          8 B/elem
-value = algorithmic bytes of all ranks / device time of K steps (CUDA events, max over
-ranks).  Inputs are 4 GiB per vector, far larger than the 126 MB L2, so no flush is
-needed between steps.  Parity of the same kernels is covered by tests/ (-m gpu); this
-script spot-checks its outputs.
+value = algorithmic bytes of all GPUs / device time of K steps.  Inputs are 4 GiB per
+vector per GPU, far larger than the 126 MB L2, so no flush is needed between steps.  Parity
+of the same kernels is covered by tests/ (-m gpu); this script spot-checks its outputs.
 
 `e2e` repeats the step through the same API from pinned host buffers: H2D of b and c,
 D2H of the triad and scan outputs, inside the timed region.  `cpu_baseline` times the
@@ -36,27 +44,70 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-BYTES = {"dot": 8, "triad": 12, "scan": 8, "copy": 8, "scale": 8, "add": 12, "black_scholes": 24}
+BYTES = {"dot": 8, "triad": 12, "scan": 8, "copy": 8, "scale": 8, "add": 12, "black_scholes": 24,
+         "scan_affine": 8, "scan_product": 12, "reduce": 4}
 KERNEL_OF = {"dot": "drk_dot", "triad": "drk_triad", "scan": "drk_scan", "copy": "drk_copy",
-             "scale": "drk_scale", "add": "drk_add", "black_scholes": "drk_black_scholes"}
+             "scale": "drk_scale", "add": "drk_add", "black_scholes": "drk_black_scholes",
+             "scan_affine": "drk_scan_view", "scan_product": "drk_scan_view", "reduce": "drk_reduce"}
 STEP_WORKLOADS = ("dot", "triad", "scan")
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--log2n", type=int, default=30, help="elements per GPU = 2^log2n (default 30)")
+    p.add_argument("--segments", type=int, default=1, help="segments (locales) per GPU (default 1)")
+    p.add_argument("--share-gpu", action="store_true",
+                   help="shp test mode: every GPU's segments on GPU 0 (also DRK_BENCH_SHARE_GPU=1)")
     p.add_argument("--workloads", default=",".join(STEP_WORKLOADS),
-                   help="comma list from dot,triad,scan,copy,scale,add,black_scholes")
+                   help="comma list from dot,triad,scan,copy,scale,add,black_scholes,scan_affine,scan_product,"
+                        "reduce")
     p.add_argument("--e2e-log2n", type=int, default=None, help="elements per GPU for e2e (default: same)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-log2n", type=int, default=26, help="CPU sample size per step (default 2^26)")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
-    return p.parse_args()
+    return p.parse_args(argv)
+
+
+def launch_mode(gpus, env=None):
+    """("spmd", world) under torchrun (WORLD_SIZE > 1), else ("shp", gpus): one process
+    driving `gpus` GPUs through one Runtime."""
+    env = os.environ if env is None else env
+    world = int(env.get("WORLD_SIZE", "1"))
+    if world > 1:
+        return "spmd", world
+    return "shp", max(1, int(gpus))
+
+
+def shp_layout(gpus, segments, visible, share=False):
+    """(devices, locales) of the single-process benchmark: `segments` locales per GPU over
+    GPUs 0..gpus-1 (locale i on devices[i % len(devices)], i.e. segment k of the vector on
+    GPU k mod gpus), or all on GPU 0 in the shared test mode."""
+    if share:
+        devices = [0]
+    else:
+        if gpus > visible:
+            raise SystemExit(f"bench.py: --gpus {gpus} but only {visible} CUDA device(s) are visible "
+                             "(DRK_BENCH_SHARE_GPU=1 runs every segment on GPU 0 as a test mode)")
+        devices = list(range(gpus))
+    return devices, gpus * segments
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 # ----------------------------------------------------------------------------------------
@@ -91,14 +142,14 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index = index
+        self.index = ",".join(str(i) for i in index) if isinstance(index, (list, tuple)) else str(index)
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                ["nvidia-smi", "-i", self.index, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -211,6 +262,14 @@ def cpu_measure(log2n, workloads, threads, min_seconds, steps=None, warmup=0):
                 O.triad(b, c, 3.0, p, threads)
             elif w == "black_scholes":
                 O.black_scholes_prices(cols, np.float32, p, threads)
+            elif w == "scan_affine":  # the reference materialises the view, then scans it
+                O.scan((np.float32(2.5) * c + np.float32(1.0)).astype(np.float32), p, np.float32, threads=threads)
+            elif w == "scan_product":
+                O.scan(b * c, p, np.float32, threads=threads)
+            elif w == "reduce":
+                O.reduce(c, p, 0.0, threads=threads)
+            else:
+                raise ValueError(f"no CPU path for workload {w!r}")
 
     for _ in range(warmup):
         step()
@@ -230,17 +289,33 @@ def cpu_measure(log2n, workloads, threads, min_seconds, steps=None, warmup=0):
     return nbytes / per_step / 1e9, per_step, len(times), n
 
 
+def reference_log2n(args):
+    """The reference arm runs the GPU arm's own size (2^log2n fp32 elements, one GPU's
+    workload) when the host has the memory for it (inputs, outputs and the numpy
+    temporaries: ~24 bytes per element), else the largest power of two that fits in half
+    of the available RAM."""
+    log2n = args.log2n
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+        while (24 << log2n) > 0.5 * avail and log2n > 20:
+            log2n -= 1
+    except Exception:
+        log2n = min(log2n, args.cpu_log2n)
+    return log2n
+
+
 def run_reference(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     workloads = [w for w in args.workloads.split(",") if w]
-    from oracle import segrange_port as O
 
     threads = len(os.sched_getaffinity(0))
-    gbs, per_step, reps, n = cpu_measure(args.cpu_log2n, workloads, threads, 0.0, steps=args.steps,
-                                         warmup=args.warmup)
+    log2n = reference_log2n(args)
+    gbs, per_step, reps, n = cpu_measure(log2n, workloads, threads, 0.0, steps=args.steps, warmup=args.warmup)
+    same = log2n == args.log2n
     line = {
         "metric": "achieved HBM GB/s (frac of roofline) for dot/triad/scan at 1/2/4/8 B200",
         "impl": "reference",
@@ -255,10 +330,15 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (splitmix64 unit doubles -> fp32, reference repro.py)",
-        "config": {"workload": "+".join(workloads) + " fp32 (reference numpy path, oracle port)",
-                   "elements_per_step": n, "segments": threads},
+        "config": {"workload": "+".join(workloads) + f" fp32, 2^{log2n} elements (reference numpy path, oracle port)",
+                   "elements_per_step": n, "segments": threads,
+                   "same_size_as_gpu_arm": same,
+                   "note": ("the GPU arm's per-GPU size" if same else
+                            f"2^{log2n} instead of the GPU arm's 2^{args.log2n}: host RAM")},
+        "elements_per_s": round(len(workloads) * n / per_step, 1),
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"2^{args.cpu_log2n} fp32 elements per step, {threads} segments/threads"},
+                         "cpu": cpu_model(),
+                         "sample": f"2^{log2n} fp32 elements per step, {threads} segments on {threads} threads"},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -268,36 +348,70 @@ def run_reference(args):
 # device path
 
 
-def main():
-    args = parse()
+class StepTimer:
+    """CUDA events on every participating GPU's stream around the timed steps; the step time
+    is the maximum over GPUs (each measured on its own device clock)."""
+
+    def __init__(self, states):
+        import torch
+
+        self.states = list(states)
+        self.ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in self.states]
+
+    def start(self):
+        for (e0, _), st in zip(self.ev, self.states):
+            e0.record(st.stream)
+
+    def stop(self):
+        for (_, e1), st in zip(self.ev, self.states):
+            e1.record(st.stream)
+
+    def ms(self):
+        for (_, e1) in self.ev:
+            e1.synchronize()
+        return max(e0.elapsed_time(e1) for e0, e1 in self.ev)
+
+
+def main(argv=None):
+    args = parse(argv)
     if args.impl == "reference":
         run_reference(args)
         return
-    world, rank, local = dist_setup(args.gpus)
+    mode, ngpu = launch_mode(args.gpus)
+    world, rank, local = dist_setup(args.gpus) if mode == "spmd" else (1, 0, 0)
     import torch
 
     import paper_2406_00158_b200 as sr
     from paper_2406_00158_b200 import _lib, algorithms as A, bench as B, kernels, repro, spmd, views
 
     workloads = [w for w in args.workloads.split(",") if w]
-    n = 1 << args.log2n
+    n = 1 << args.log2n                       # elements per GPU
     dt = np.float32
-    rt = sr.Runtime(1, devices=[local])
-    st = rt.device_state(local)
-    group = spmd.Group() if world > 1 else None
+    share = args.share_gpu or os.environ.get("DRK_BENCH_SHARE_GPU") == "1"
+    if mode == "shp":
+        devices, locales = shp_layout(ngpu, args.segments, torch.cuda.device_count(), share)
+        rt = sr.Runtime(locales, devices=devices)
+        N = n * ngpu                          # the global vector
+        off = 0
+    else:
+        rt = sr.Runtime(args.segments, devices=[local])
+        N = n * world
+        off = rank * n                        # this rank's block of the global vector
+    states = rt.device_states
+    vlen = N if mode == "shp" else n
+    group = spmd.Group() if mode == "spmd" else None
 
-    a = sr.DistributedVector(rt, n, dtype=dt)
-    b = sr.DistributedVector(rt, n, dtype=dt)
-    c = sr.DistributedVector(rt, n, dtype=dt)
-    N = n * world
-    repro.fill_unit(b, 1, rank * n)          # global vector b = unit_doubles(1, 0, N)
-    repro.fill_unit(c, 1, N + rank * n)      # global vector c = unit_doubles(1, N, N)
+    a = sr.DistributedVector(rt, vlen, dtype=dt)
+    b = sr.DistributedVector(rt, vlen, dtype=dt)
+    c = sr.DistributedVector(rt, vlen, dtype=dt)
+    repro.fill_unit(b, 1, off)          # global vector b = unit_doubles(1, 0, N)
+    repro.fill_unit(c, 1, N + off)      # global vector c = unit_doubles(1, N, N)
     bs_cols = None
     if "black_scholes" in workloads:
         bs_cols = []
         for k, (lo, hi) in enumerate(B.BS_RANGES.values()):
-            v = sr.DistributedVector(rt, n, dtype=dt)
-            repro.fill_uniform(v, 1, k * N + rank * n, lo, hi)
+            v = sr.DistributedVector(rt, vlen, dtype=dt)
+            repro.fill_uniform(v, 1, k * N + off, lo, hi)
             bs_cols.append(v)
 
     results = {}
@@ -321,6 +435,12 @@ def main():
             B.stream_add(a, b, c)
         elif w == "black_scholes":
             B.black_scholes_prices(a, *bs_cols)
+        elif w == "scan_affine":  # inclusive_scan(transform(c, 2.5 c + 1)): fused, 8 B/elem
+            A.inclusive_scan(views.transform(c, lambda x: 2.5 * x + 1.0), a)
+        elif w == "scan_product":  # inclusive_scan(transform(zip(b, c), t0 * t1)): fused, 12 B/elem
+            A.inclusive_scan(views.transform(views.zip(b, c), lambda t: t[0] * t[1]), a)
+        elif w == "reduce":
+            results["reduce"] = A.reduce(c, 0.0, A.add)
 
     def step():
         for w in workloads:
@@ -328,25 +448,26 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize(local)
+    rt.synchronize()
     barrier(world)
     launches0 = _lib.launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    timer = StepTimer(states)
+    with ClockSampler(sorted({st.index for st in states})) as clocks:
         with kernels.profile() as prof:
-            torch.cuda.synchronize(local)
-            ev0.record(st.stream)
+            rt.synchronize()
+            timer.start()
             for _ in range(args.steps):
                 step()
-            ev1.record(st.stream)
-            torch.cuda.synchronize(local)
+            timer.stop()
+            rt.synchronize()
     barrier(world)
     launches = _lib.launch_count() - launches0
-    ms = ev0.elapsed_time(ev1)
-    ms = max_over_ranks(ms, world)
+    ms = max_over_ranks(timer.ms(), world)
     ms_step = ms / args.steps
-    step_bytes = sum(BYTES[w] for w in workloads) * n
-    value = step_bytes * world / (ms_step / 1e3) / 1e9
+    gpus_total = ngpu if mode == "shp" else world
+    elems_total = n * gpus_total              # elements of each pipeline, all GPUs
+    step_bytes = sum(BYTES[w] for w in workloads) * elems_total
+    value = step_bytes / (ms_step / 1e3) / 1e9
     peak, peak_src = peaks()
 
     # per-kernel live timing (CUDA events on the launch stream, inside the timed region)
@@ -361,13 +482,15 @@ def main():
         avg_bytes = BYTES[w] * elems / cnt
         gbs = avg_bytes / (avg_ms / 1e3) / 1e9
         per[w] = {"kernel": name, "launches": cnt, "avg_ms": round(avg_ms, 4), "GB/s": round(gbs, 1),
+                  "elements_per_s": round(elems / cnt / (avg_ms / 1e3), 1),
                   "frac": round(gbs / peak, 4), "bytes_per_launch": int(avg_bytes)}
     dom = max(per, key=lambda w: per[w]["avg_ms"] * per[w]["launches"]) if per else None
     traffic_db = ncu_traffic()
     roofline = None
     if dom:
         tr = traffic_db.get(per[dom]["kernel"], {})
-        traffic = tr.get("dram_bytes_per_launch") if tr.get("elements") == n else None
+        traffic = tr.get("dram_bytes_per_launch") if tr.get("elements") == per[dom]["bytes_per_launch"] // BYTES[dom] \
+            else None
         roofline = {"bound": "hbm", "kernel": per[dom]["kernel"], "achieved": per[dom]["GB/s"], "peak": peak,
                     "peak_source": peak_src, "unit": "GB/s", "frac": per[dom]["frac"],
                     "algorithmic_bytes_per_launch": per[dom]["bytes_per_launch"], "traffic": traffic}
@@ -381,23 +504,34 @@ def main():
     # ---- end to end through the API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, rt, st, world, rank, group, workloads, dt)
+        e2e = run_e2e(args, rt, world, rank, group, workloads, dt, ngpu if mode == "shp" else 1)
 
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and gpus_total == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
         gbs, per_step, reps, ncpu = cpu_measure(args.cpu_log2n, workloads, threads, args.cpu_seconds)
-        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port", "cpu": cpu_model(),
                "sample": f"{reps} steps of 2^{args.cpu_log2n} fp32 elements ({'+'.join(workloads)}), "
                          f"{threads} segments on {threads} threads, median {per_step * 1e3:.1f} ms/step"}
 
     if rank == 0:
+        cfg = {"workload": "+".join(workloads) + f" fp32, 2^{args.log2n} elements per GPU",
+               "mode": mode + (" (shared GPU 0: test mode, not a measurement)" if share and mode == "shp" else ""),
+               "elements_per_gpu": n, "global_elements": elems_total, "segments_per_gpu": args.segments,
+               "devices": [st.index for st in states] if mode == "shp" else None,
+               "parallelism": f"dp{gpus_total}",
+               "l2": (f"inputs {n * 4 / 2**30:.3g} GiB per vector per GPU = {n * 4 / 126e6:.3g}x the 126 MB L2"
+                      + (" (no flush needed)" if n * 4 > 4 * 126e6 else " (L2-resident: not a DRAM number)")),
+               "frac_of_aggregate_roofline": round(value / (peak * gpus_total), 4)}
+        if "scan" in workloads and gpus_total > 1:
+            cfg["scan_note"] = ("with the vector spread over GPUs the scan is reduce-then-scan: 12 B/elem of traffic "
+                                "against 8 B/elem algorithmic, so its roofline fraction is capped near 2/3")
         line = {
             "metric": "achieved HBM GB/s (frac of roofline) for dot/triad/scan at 1/2/4/8 B200",
             "value": round(value, 2),
             "unit": "GB/s",
-            "n_gpus": world,
+            "n_gpus": gpus_total,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(ms_step, 4),
@@ -406,11 +540,8 @@ def main():
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (splitmix64 unit doubles -> fp32, generated on device, reference repro.py)",
-            "config": {"workload": "+".join(workloads) + f" fp32, 2^{args.log2n} elements per GPU",
-                       "elements_per_gpu": n, "segments_per_gpu": 1, "parallelism": f"dp{world}",
-                       "l2": (f"inputs {n * 4 / 2**30:.3g} GiB per vector = {n * 4 / 126e6:.3g}x the 126 MB L2"
-                              + (" (no flush needed)" if n * 4 > 4 * 126e6 else " (L2-resident: not a DRAM number)")),
-                       "frac_of_aggregate_roofline": round(value / (peak * world), 4)},
+            "config": cfg,
+            "elements_per_s": round(len(workloads) * elems_total / (ms_step / 1e3), 1),
             "roofline": roofline,
             "workloads": per,
             "gpu_launches": int(launches),
@@ -420,33 +551,35 @@ def main():
             "checks": checks,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if mode == "spmd":
         import torch.distributed as dist
 
         dist.destroy_process_group()
 
 
-def run_e2e(args, rt, st, world, rank, group, workloads, dt):
+def run_e2e(args, rt, world, rank, group, workloads, dt, ngpu=1):
     """The step through the public API from pinned host memory: uploads of b and c, the
     three pipelines, downloads of the triad and scan outputs (and the dot scalar), every
     step.  Transfers use the asynchronous API (upload/to_numpy with wait=False) on
     double-buffered device vectors, so step i+1's host->device copies overlap step i's
-    device->host copies — the two PCIe directions — and the kernels wait on the device."""
+    device->host copies — the two PCIe directions — and the kernels wait on the device.
+    In shp mode every GPU's segment moves over its own PCIe link concurrently."""
     import torch
 
     import paper_2406_00158_b200 as sr
     from paper_2406_00158_b200 import algorithms as A, bench as B, spmd, views
 
     log2n = args.e2e_log2n if args.e2e_log2n is not None else args.log2n
+    gpus = ngpu * world
     try:
         import psutil
 
         avail = psutil.virtual_memory().available
-        while (4 << log2n) * 4 * world > 0.4 * avail and log2n > 20:
+        while (4 << log2n) * 4 * gpus > 0.4 * avail and log2n > 20:
             log2n -= 1
     except Exception:
         pass
-    n = 1 << log2n
+    n = (1 << log2n) * ngpu  # this process's vector length
     hb, hc = sr.pinned_empty(n, dt), sr.pinned_empty(n, dt)
     ha, ho = sr.pinned_empty(n, dt), sr.pinned_empty(n, dt)
     rng = np.random.default_rng(rank)
@@ -480,20 +613,20 @@ def run_e2e(args, rt, st, world, rank, group, workloads, dt):
     step(0)
     step(1)
     drain()
-    torch.cuda.synchronize()
+    rt.synchronize()
     barrier(world)
     steps = max(3, min(args.steps, 10))
     t0 = time.perf_counter()
     for i in range(steps):
         step(i)
     drain()
-    torch.cuda.synchronize()
+    rt.synchronize()
     dtm = (time.perf_counter() - t0) / steps
     dtm = max_over_ranks(dtm, world)
     nbytes = sum(BYTES[w] for w in sw) * n * world
     del sets
     return {"value": round(nbytes / dtm / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "elements_per_gpu": n, "ms_per_step": round(dtm * 1e3, 3),
+            "d2h_bytes_per_step": d2h, "elements_per_gpu": n // ngpu, "ms_per_step": round(dtm * 1e3, 3),
             "note": "same step via the public API from pinned host memory; every step uploads b and c and "
                     "downloads both outputs (+ the dot scalar) inside the timed region; async transfers on "
                     "double-buffered vectors overlap the two PCIe directions (wall clock, max over ranks)"}

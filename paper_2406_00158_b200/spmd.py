@@ -88,6 +88,13 @@ def _decode(bits, A):
     return np.asarray(np.array([bits], dtype=np.int64).view(wide)[0]).astype(A)[()]
 
 
+# dtypes a gathered value can carry; the pair's has-word is 1 + the sender's dtype index, so
+# every rank decodes every value in its sender's dtype (a rank without elements does not
+# know the dtype of the others' partials)
+_PAIR_DTYPES = [np.dtype(d) for d in (np.float32, np.float64, np.int32, np.int64, np.uint32, np.uint64,
+                                      np.int16, np.int8, np.uint16, np.uint8, np.float16, np.bool_)]
+
+
 def gather_pairs(value, acc_dtype, group: Group, state=None) -> list:
     """All-gather of one optional value per rank -> list indexed by rank (None = that rank
     had no elements).  With NCCL the (has, value) pair is written by a kernel, gathered on
@@ -98,7 +105,7 @@ def gather_pairs(value, acc_dtype, group: Group, state=None) -> list:
     A = np.dtype(acc_dtype)
     pair = np.zeros(2, dtype=np.int64)
     if value is not None:
-        pair[0], pair[1] = 1, _encode(value, A)
+        pair[0], pair[1] = 1 + _PAIR_DTYPES.index(A), _encode(value, A)
     if group.backend == "nccl" and state is not None:
         with t.cuda.stream(state.stream):
             buf = t.empty(2, dtype=t.int64, device=state.device)
@@ -117,7 +124,7 @@ def gather_pairs(value, acc_dtype, group: Group, state=None) -> list:
         outs = t.empty(2 * group.size, dtype=t.int64, device=x.device)
         dist.all_gather_into_tensor(outs, x, group=group.group)
         got = outs.cpu().numpy().reshape(group.size, 2)
-    return [_decode(v, A) if h else None for h, v in got]
+    return [_decode(v, _PAIR_DTYPES[h - 1]) if h else None for h, v in got]
 
 
 def allreduce_partial(partial, opname: str, acc_dtype, group: Group, state=None):
