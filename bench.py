@@ -46,9 +46,12 @@ sys.path.insert(0, ROOT)
 
 BYTES = {"dot": 8, "triad": 12, "scan": 8, "copy": 8, "scale": 8, "add": 12, "black_scholes": 24,
          "scan_affine": 8, "scan_product": 12, "reduce": 4}
-KERNEL_OF = {"dot": "drk_dot", "triad": "drk_triad", "scan": "drk_scan", "copy": "drk_copy",
-             "scale": "drk_scale", "add": "drk_add", "black_scholes": "drk_black_scholes",
-             "scan_affine": "drk_scan_view", "scan_product": "drk_scan_view", "reduce": "drk_reduce"}
+# the libdrk entry points each pipeline launches (kernels.profile keys; batched variants run
+# when a GPU holds several segments)
+KERNEL_OF = {"dot": ("drk_dot", "drk_dot_batch"), "triad": ("drk_triad",), "scan": ("drk_scan", "drk_scan_batch"),
+             "copy": ("drk_copy",), "scale": ("drk_scale",), "add": ("drk_add",),
+             "black_scholes": ("drk_black_scholes",), "scan_affine": ("drk_scan_view:affine",),
+             "scan_product": ("drk_scan_view:product",), "reduce": ("drk_reduce", "drk_reduce_batch")}
 STEP_WORKLOADS = ("dot", "triad", "scan")
 
 
@@ -474,10 +477,11 @@ def main(argv=None):
     ksum = prof.summary()
     per = {}
     for w in workloads:
-        name = KERNEL_OF[w]
-        if name not in ksum:
+        names = [k for k in KERNEL_OF[w] if k in ksum]
+        if not names:
             continue
-        cnt, kms, elems = ksum[name]
+        name = names[0] if len(names) == 1 else "+".join(names)
+        cnt, kms, elems = (sum(ksum[k][i] for k in names) for i in range(3))
         avg_ms = kms / cnt
         avg_bytes = BYTES[w] * elems / cnt
         gbs = avg_bytes / (avg_ms / 1e3) / 1e9

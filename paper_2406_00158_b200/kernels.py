@@ -48,8 +48,9 @@ class profile:
         return out
 
 
-def launch_kernel(name, launch_ctx, n, *args):
-    """Call libdrk entry `name` (device and stream appended) on launch_ctx."""
+def launch_kernel(name, launch_ctx, n, *args, key=None):
+    """Call libdrk entry `name` (device and stream appended) on launch_ctx; `key` names the
+    launch in kernels.profile (default: the entry point, drk_*_ex reported without _ex)."""
     if _PROFILE is None:
         _lib.call(name, *args, launch_ctx.device, launch_ctx.stream)
         return
@@ -60,7 +61,8 @@ def launch_kernel(name, launch_ctx, n, *args):
     s.record(launch_ctx.state.stream)
     _lib.call(name, *args, launch_ctx.device, launch_ctx.stream)
     e.record(launch_ctx.state.stream)
-    key = name[:-3] if name.endswith("_ex") else name  # drk_scan_ex is reported as drk_scan
+    if key is None:
+        key = name[:-3] if name.endswith("_ex") else name  # drk_scan_ex is reported as drk_scan
     _PROFILE.setdefault(key, []).append((s, e, n))
 
 
@@ -440,7 +442,8 @@ def run_scan_view(T, opcode, exclusive, view: ScanView, out_ptr, n, lctx: Launch
         nbytes = _scan_scratch_bytes(code, opcode, n)
         scratch = st.scan_scratch(nbytes, scratch_index)
         launch_kernel("drk_scan_view_ex", lctx, n, kind, code, opcode, *tail, flags, wbuf, len(words),
-                      1 if view.vec_ok() else 0, *common, scratch.data_ptr(), scratch.numel())
+                      1 if view.vec_ok() else 0, *common, scratch.data_ptr(), scratch.numel(),
+                      key="drk_scan_view:" + ("product" if kind == _lib.VIEW_PRODUCT else "affine"))
         return
     from . import codegen
 
@@ -460,7 +463,7 @@ def run_scan_view(T, opcode, exclusive, view: ScanView, out_ptr, n, lctx: Launch
     s_.record(st.stream)
     _lib.call("drk_jit_scan_view", *args)
     e_.record(st.stream)
-    _PROFILE.setdefault("drk_scan", []).append((s_, e_, n))
+    _PROFILE.setdefault("drk_scan_view:jit", []).append((s_, e_, n))
 
 
 def _scan_scratch_bytes(code, opcode, n):

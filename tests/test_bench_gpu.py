@@ -45,4 +45,5 @@ def test_bench_c1_named_workload():
 def test_bench_fused_scan_workloads():
     d = _bench("--workloads", "scan_affine,scan_product", "--log2n", "24", "--steps", "5", "--warmup", "3",
                "--no-cpu", "--no-e2e")
-    assert d["workloads"]["scan_affine"]["launches"] == 10  # both fused scans report as drk_scan_view
+    assert d["workloads"]["scan_affine"]["launches"] == 5 and d["workloads"]["scan_product"]["launches"] == 5
+    assert d["workloads"]["scan_product"]["kernel"] == "drk_scan_view:product"
