@@ -243,13 +243,16 @@ int drk_jit_scan(void* handle, const char* kernel, int acc_bytes, int tile, int 
                  const void* in, void* out, int64_t n, const void* init_host, const void* carry_host,
                  const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
                  size_t scratch_bytes, int device, void* stream);
-/* scan of a fused view with an NVRTC module that defines drk_scan_l2_4, drk_scan_l2_8 and
- * drk_scan_1p over its generated loader (value size v_bytes, accumulator size acc_bytes):
- * arguments as drk_scan_view_ex; scratch of drk_jit_scan_scratch_bytes(n, 256 * items). */
-int drk_jit_scan_view(void* handle, int v_bytes, int acc_bytes, int exclusive, int flags, const uint64_t* words,
-                      int nwords, int vec_ok, void* out, int64_t n, const void* init_host, const void* carry_host,
-                      const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
-                      size_t scratch_bytes, int device, void* stream);
+/* scan of a fused view with an NVRTC module that defines drk_scan_l2_s / drk_scan_l2_l (the L2
+ * scan over its generated loader with `items` elements per thread and subs_small / subs_large
+ * sub-tiles, nl staged leaves — 0 for a register loader) and drk_scan_1p (single pass,
+ * items_1p per thread), for values of v_bytes and an accumulator of acc_bytes: other
+ * arguments as drk_scan_view_ex; scratch of drk_jit_scan_scratch_bytes(n, 256 * items_1p). */
+int drk_jit_scan_view(void* handle, int v_bytes, int acc_bytes, int items, int nl, int subs_small, int subs_large,
+                      int items_1p, int exclusive, int flags, const uint64_t* words, int nwords, int vec_ok,
+                      void* out, int64_t n, const void* init_host, const void* carry_host, const void* carry_dev,
+                      void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,
+                      void* stream);
 const char* drk_jit_last_error(void);
 int64_t drk_note_launch(void);
 

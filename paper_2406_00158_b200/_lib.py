@@ -89,8 +89,8 @@ SIGNATURES = {
                              _vp, _vp, _sz, _int, _vp]),
     "drk_scan_view_ex": (_int, [_int, _int, _int, _int, _int, ctypes.POINTER(_u64), _int, _int, _vp, _i64, _vp, _vp,
                                 _vp, _vp, _vp, _vp, _sz, _int, _vp]),
-    "drk_jit_scan_view": (_int, [_vp, _int, _int, _int, _int, ctypes.POINTER(_u64), _int, _int, _vp, _i64, _vp, _vp,
-                                 _vp, _vp, _vp, _vp, _sz, _int, _vp]),
+    "drk_jit_scan_view": (_int, [_vp, _int, _int, _int, _int, _int, _int, _int, _int, _int, ctypes.POINTER(_u64),
+                                 _int, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "drk_carry_fold": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _vp, _vp, _vp, _int,
                               _vp]),
     "drk_sort_keys": (_int, [_int, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),

@@ -743,11 +743,12 @@ _SCAN_VIEW_PLANS = {}
 
 
 def scan_view_plan(view, T, opcode, combiner=None):
-    """(module, words, items) of the fused scan of `view` (kernels.ScanView: node already cast
-    to the output dtype T) with a libdrk operator or a traced custom combiner.  The module
-    defines drk_scan_l2_4 / drk_scan_l2_8 / drk_scan_1p over a generated loader whose
+    """(module, words, geometry) of the fused scan of `view` (kernels.ScanView: node already
+    cast to the output dtype T) with a libdrk operator or a traced custom combiner.  The
+    module defines drk_scan_l2_s / drk_scan_l2_l / drk_scan_1p over a generated loader whose
     parameters are JitWords: one word per used leaf (pointer or index base), then constants
-    (kernel parameters, so expressions differing only in constants share one module)."""
+    (kernel parameters, so expressions differing only in constants share one module).
+    geometry = (items, nl, subs_small, subs_large, items_1p) for drk_jit_scan_view."""
     T = np.dtype(T)
     node, leaves = view.node, view.leaves
     fk = expr._fn_key(combiner.fn) if combiner is not None else None
@@ -761,11 +762,20 @@ def scan_view_plan(view, T, opcode, combiner=None):
             if len(_SCAN_VIEW_PLANS) >= _PLAN_MAX:
                 _SCAN_VIEW_PLANS.clear()
             _SCAN_VIEW_PLANS[key] = plan
-    mod, wvals, leaf_w, items = plan
+    mod, wvals, leaf_w, geom = plan
     words = list(wvals)
     for k, w in leaf_w.items():
         words[w] = view.ptrs[k] if leaves[k].kind != "index" else leaves[k].base
-    return mod, words, items
+    return mod, words, geom
+
+
+def scan_geometry(T, nl):
+    """drk_device.cuh ScanGeom: (items, subs_small, subs_large) of the L2 scan for values of
+    dtype T and nl staged leaves."""
+    four = np.dtype(T).itemsize == 4
+    if nl >= 2:
+        return (12 if four else 6), 3, 7
+    return (20 if four else 10), 4, 8
 
 
 def _scan_view_plan(node, leaves, T, opcode, combiner, used):
@@ -776,12 +786,19 @@ def _scan_view_plan(node, leaves, T, opcode, combiner, used):
             combiner = None
     opname, opsrc = _op_struct(opcode, combiner, T)
     array_slots = [k for k in used if leaves[k].kind in ("array", "host")]
+    # staged (TMA through the ring, values computed in shared memory) when the view reads one
+    # or two arrays of the value's element size; otherwise a register loader
+    staged = 1 <= len(array_slots) <= 2 and all(leaves[k].dtype.itemsize == T.itemsize for k in array_slots)
+    nl = len(array_slots) if staged else 0
+    raw_of = {k: r for r, k in enumerate(array_slots)}
     words = Words()
     leaf_w = {k: words.add(0) for k in used}
 
     def lv(k):
         if leaves[k].kind == "index":
             return f"(long long)(p.w[{leaf_w[k]}] + gi)"
+        if staged:
+            return f"drk::bits_as<{ctype(leaves[k].dtype)}>(raw[{raw_of[k]}][e])"
         return f"a{k}[e]"
 
     def ls(k):
@@ -797,18 +814,29 @@ def _scan_view_plan(node, leaves, T, opcode, combiner, used):
     if len(words.values) > _lib.JIT_WORDS:
         raise JitError(f"fused scan needs {len(words.values)} parameter words (max {_lib.JIT_WORDS})")
     V = ctype(T)
-    items = _scan_items(T)
-    loads = "\n".join(f"    {ctype(leaves[k].dtype)} a{k}[E];\n    drk::ldv_hint<{ctype(leaves[k].dtype)}, E>("
-                      f"(const {ctype(leaves[k].dtype)}*)p.w[{leaf_w[k]}] + i, a{k}, pol);" for k in array_slots)
-    nl = "\n      "
+    items, subs_small, subs_large = scan_geometry(T, nl)
+    items_1p = _scan_items(T)
+    nl_ = "\n      "
     nl4 = "\n    "
-    params = f"drk::ScanParams<typename drk::WideAcc<{V}, {opname}>::type, drk::JitWords>"
-    src = f'''#include "drk_device.cuh"
-{opsrc}
-struct LD {{
-  typedef {V} V;
-  typedef drk::JitWords Params;
-  static constexpr bool bulk = false;
+    if staged:
+        leaf_sel = " : ".join(f"k == {r} ? p.w[{leaf_w[k]}]" for r, k in enumerate(array_slots)) + " : 0ull"
+        body = f'''  typedef typename drk::RawOf<V>::type R;
+  static constexpr int NL = {nl};
+  static __device__ __forceinline__ const void* leaf(const Params& p, int k) {{ return (const void*)({leaf_sel}); }}
+  template <int E>
+  static __device__ __forceinline__ void compute(const Params& p, const R (&raw)[NL][E], long long gi0, V (&v)[E]) {{
+#pragma unroll
+    for (int e = 0; e < E; ++e) {{
+      const long long gi = gi0 + e;
+      (void)gi;
+      {nl_.join(ev.lines)}
+      v[e] = (V)({rv});
+    }}
+  }}'''
+    else:
+        loads = "\n".join(f"    {ctype(leaves[k].dtype)} a{k}[E];\n    drk::ldv_hint<{ctype(leaves[k].dtype)}, E>("
+                          f"(const {ctype(leaves[k].dtype)}*)p.w[{leaf_w[k]}] + i, a{k}, pol);" for k in array_slots)
+        body = f'''  static constexpr int NL = 0;
   static constexpr int E = 16 / sizeof(V);
   static __device__ __forceinline__ void load16(const Params& p, long long i, V (&v)[E], unsigned long long pol) {{
 {loads}
@@ -816,27 +844,35 @@ struct LD {{
     for (int e = 0; e < E; ++e) {{
       const long long gi = i + e;
       (void)gi;
-      {nl.join(ev.lines)}
+      {nl_.join(ev.lines)}
       v[e] = (V)({rv});
     }}
-  }}
+  }}'''
+    params = f"drk::ScanParams<typename drk::WideAcc<{V}, {opname}>::type, drk::JitWords>"
+    src = f'''#include "drk_device.cuh"
+{opsrc}
+struct LD {{
+  typedef {V} V;
+  typedef drk::JitWords Params;
+  static constexpr bool bulk = false;
+{body}
   static __device__ __forceinline__ V one(const Params& p, long long i) {{
     {nl4.join(es.lines)}
     return (V)({rs});
   }}
 }};
-extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_l2_4(const {params} p) {{
-  drk::scan_l2_body<LD, {opname}, {BLOCK}, {items}, 4, 3>(p);
+extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_l2_s(const {params} p) {{
+  drk::scan_l2_body<LD, {opname}, {BLOCK}, {items}, {subs_small}, 3>(p);
 }}
-extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_l2_8(const {params} p) {{
-  drk::scan_l2_body<LD, {opname}, {BLOCK}, {items}, 8, 3>(p);
+extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_l2_l(const {params} p) {{
+  drk::scan_l2_body<LD, {opname}, {BLOCK}, {items}, {subs_large}, 3>(p);
 }}
 extern "C" __global__ void __launch_bounds__({BLOCK}) drk_scan_1p(const {params} p) {{
-  drk::scan_kernel_body<LD, {V}, {opname}, {BLOCK}, {items}, 3>(p);
+  drk::scan_kernel_body<LD, {V}, {opname}, {BLOCK}, {items_1p}, 3>(p);
 }}
 '''
     mod = compile_module(src, "drk_scan_view.cu")
-    return (mod, list(words.values), leaf_w, items)
+    return (mod, list(words.values), leaf_w, (items, nl, subs_small, subs_large, items_1p))
 
 
 class _SegList:

@@ -15,8 +15,7 @@
 #include <string>
 #include <unordered_map>
 
-#include "../../include/drk.h"
-#include "drk_device.cuh"
+#include "drk_host.h"
 
 using namespace drk;
 
@@ -26,19 +25,17 @@ using namespace drk;
 static thread_local std::string g_last_error;
 static std::atomic<int64_t> g_launches{0};
 
-static int set_error(int code, const std::string& msg) {
+namespace drk_host {
+int set_error(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
-static int cuda_status(cudaError_t e, const char* what) {
+int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return 0;
   return set_error((int)e, std::string(what) + ": " + cudaGetErrorString(e));
 }
-#define DRK_CHECK(call)                                  \
-  do {                                                   \
-    cudaError_t _e = (call);                             \
-    if (_e != cudaSuccess) return cuda_status(_e, #call); \
-  } while (0)
+}  // namespace drk_host
+using namespace drk_host;
 
 extern "C" const char* drk_last_error(void) { return g_last_error.c_str(); }
 int drk_error(int code, const char* msg) { return set_error(code, msg); }
@@ -129,26 +126,48 @@ extern "C" int drk_device_count(int* count) {
 }
 
 // ---------------------------------------------------------------------------------------
-// launch geometry
+// launch geometry and knobs (declared in drk_host.h)
 
-static constexpr int BLOCK = 256;
-static constexpr int MAP_U = 4;
-static constexpr int RED_U = 4;
-static constexpr int MAX_RED_GRID = 4096;
+namespace drk_host {
+std::mutex g_mu;
+int g_map_waves = 0;
+int g_reduce_waves = 1;
+int g_scan_sub = 3;
+int g_scan_l2dyn = 1;
+int g_scan_l2_min = 1 << 22;
+int g_scan_l2_subs = 0;
+int g_scan_l2_pre = 2;
+int g_scan_l2_ring = 3;
+int g_scan_debug = 0;
+int g_scan_stagger = -1;
+thread_local int g_chain_launch = 0;
+void* g_scan_trace = nullptr;
 
-static std::mutex g_mu;
-static int g_map_waves = 0;     // 0: size grid to cover the work once (non-persistent)
-static int g_reduce_waves = 1;  // reduce grid = SMs * occupancy * waves
-static int g_scan_sub = 3;       // scan sub-tiles per CTA tile (1..4)
-static int g_scan_l2dyn = 1;     // L2-resident two-touch scan for large aligned segments
-static int g_scan_l2_min = 1 << 22;
-static int g_scan_l2_subs = 0;   // sub-tiles per L2 tile (0: 8 = 160 KB for 4-byte types)
-static int g_scan_l2_pre = 2;    // sub-tiles scanned prefix-free during the look-back
-static int g_scan_l2_ring = 3;   // TMA ring slots of the L2 re-scan (2 or 3)
-static int g_scan_debug = 0;     // ScanParams::debug (experiments only)
-static int g_scan_stagger = -1;  // ns between first-wave tile starts of the L2 scan (-1: automatic)
-static thread_local int g_chain_launch = 0;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
-static void* g_scan_trace = nullptr;  // debug: per-tile timestamps of the next scans
+int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+int epilogue(const char* what) {
+  g_launches.fetch_add(1);
+  return cuda_status(cudaGetLastError(), what);
+}
+
+// Per-scratch launch epochs (tile descriptors of older launches then read as stale).
+static std::unordered_map<uintptr_t, uint64_t> g_scan_epochs;
+uint64_t next_epoch(void* scratch) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return ++g_scan_epochs[(uintptr_t)scratch];
+}
+}  // namespace drk_host
+
 extern "C" int drk_scan_set_trace(void* buf) {
   g_scan_trace = buf;
   return 0;
@@ -190,46 +209,6 @@ extern "C" int drk_tune(const char* name, int value) {
     if (value >= 1 && value <= 4) g_scan_sub = value;
   }
   return old;
-}
-
-static int sm_count(int device) {
-  static int cache[64] = {0};
-  if (device < 0 || device >= 64) return 148;
-  if (!cache[device]) {
-    int v = 0;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
-      v = 148;
-    cache[device] = v;
-  }
-  return cache[device];
-}
-
-template <class K> static int occupancy(K kernel, int block, size_t smem) {
-  static std::unordered_map<const void*, int> cache;
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = cache.find((const void*)kernel);
-  if (it != cache.end()) return it->second;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, smem) != cudaSuccess || n < 1)
-    n = 1;
-  cache[(const void*)kernel] = n;
-  return n;
-}
-
-static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
-
-static int prologue(int device, const char* what) {
-  int cur = -1;
-  if (cudaGetDevice(&cur) != cudaSuccess || cur != device) {
-    cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) return cuda_status(e, what);
-  }
-  return 0;
-}
-
-static int epilogue(const char* what) {
-  g_launches.fetch_add(1);
-  return cuda_status(cudaGetLastError(), what);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -461,22 +440,6 @@ static int launch_map(const typename F::Params& p, int64_t n, bool vec_ok, int d
   }
   return epilogue(what);
 }
-
-#define DRK_DISPATCH(dtype, what, T, ...)                                         \
-  switch (dtype) {                                                               \
-    case DRK_F32: { typedef float T; __VA_ARGS__; }                              \
-    case DRK_F64: { typedef double T; __VA_ARGS__; }                             \
-    case DRK_I32: { typedef int T; __VA_ARGS__; }                                \
-    case DRK_I64: { typedef long long T; __VA_ARGS__; }                          \
-    default: return set_error(DRK_E_DTYPE, std::string(what) + ": unknown dtype"); \
-  }
-
-#define DRK_DISPATCH_FLOAT(dtype, what, T, ...)                                       \
-  switch (dtype) {                                                                   \
-    case DRK_F32: { typedef float T; __VA_ARGS__; }                                  \
-    case DRK_F64: { typedef double T; __VA_ARGS__; }                                 \
-    default: return set_error(DRK_E_DTYPE, std::string(what) + ": needs float32/float64"); \
-  }
 
 static int need(const void* p, const char* what, const char* arg) {
   if (!p) return set_error(DRK_E_ARG, std::string(what) + ": null " + arg);
@@ -758,484 +721,6 @@ extern "C" int drk_dot(int dtype, const void* x, const void* y, int64_t n, void*
     return launch_reduce<ProdLoad<T>, OpAdd>(p, n, aligned16(x) && aligned16(y), result_dev, scratch, device,
                                              stream, "drk_dot");
   });
-}
-
-// ---------------------------------------------------------------------------------------
-// scans
-
-template <class T, class Op> struct ScanItems {
-  // ITEMS * sizeof(T) / 16 odd => conflict-free 16-byte LDS of per-thread runs.
-  // (int32 sums keep 64-bit running partials; 20 still fits without spills: 64 registers)
-  static constexpr int value = sizeof(T) == 4 ? 20 : 10;
-};
-
-template <class T, class Op> static size_t scan_scratch(int64_t n) {
-  // sized for the smallest tile (SUB = 1) so any g_scan_sub fits
-  constexpr int TILE = BLOCK * ScanItems<T, Op>::value;
-  const size_t nt = (size_t)((n + TILE - 1) / TILE);
-  return 128 + nt * 16;
-}
-
-// Per-scratch launch epochs (tile descriptors of older launches then read as stale).
-static std::unordered_map<uintptr_t, uint64_t> g_scan_epochs;
-static uint64_t next_epoch(void* scratch) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  return ++g_scan_epochs[(uintptr_t)scratch];
-}
-
-// Launch an L2-scan kernel (AOT template instance or NVRTC kernel, given as a function
-// pointer) over ntiles tiles: stagger and early-trigger policy, and the programmatic-
-// dependent launch of a chained segment scan (drk_scan_ex DRK_SCAN_CHAINED).
-template <class A, class LP>
-static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int smem, int device, cudaStream_t s) {
-  const int64_t nt = (p.n + tile - 1) / tile;
-  if (nt > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
-  p.ntiles = (u32)nt;
-  DRK_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  // With more than two waves of tiles, every CTA lets a chained successor launch as soon as
-  // it starts (a no-op unless the next kernel is a DRK_SCAN_CHAINED scan): all of this grid
-  // has started only after most of it has finished, i.e. after its own wait for the scan
-  // before it, whose scratch the successor reuses.
-  const int64_t wave = (int64_t)sm_count(device) * occupancy(fn, BLOCK, smem);
-  p.early_trigger = nt > 2 * wave;
-  // Stagger the first wave's reduces (ticket order) when the grid spans several waves:
-  // 2^26-2^28 elements gain 4-6 %; a single wave gains nothing (all tiles must be read
-  // before the last look-back resolves anyway)
-  p.stagger_tiles = (u32)wave;
-  if (g_scan_stagger < 0) p.stagger_ns = nt > 2 * wave ? 40 : 0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)nt);
-  cfg.blockDim = dim3(BLOCK);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  if (g_chain_launch) {
-    // programmatic dependent of the previous scan of the chain (see carry_dev_read)
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
-  void* args[] = {&p};
-  DRK_CHECK(cudaLaunchKernelExC(&cfg, fn, args));
-  return 0;
-}
-
-// 160 KB tiles (8 x 20 KB for 4-byte types); below 2^25 elements (about one wave of tiles)
-// 80 KB tiles, which give the grid more waves (2^23: 32.8 -> 26.9 us).  Other tile sizes
-// measured (3, 6, 7, 10, 12 sub-tiles) are not instantiated.
-static int l2_subs(int64_t n) { return g_scan_l2_subs == 4 || g_scan_l2_subs == 8 ? g_scan_l2_subs
-                                                                                   : (n < ((int64_t)1 << 25) ? 4 : 8); }
-
-template <class LDR, class Op>
-static int launch_scan_l2_any(ScanParams<typename WideAcc<typename LDR::V, Op>::type, typename LDR::Params>& p,
-                              int device, cudaStream_t s) {
-  typedef typename LDR::V T;
-  constexpr int IT = ScanItems<T, Op>::value;
-  const int subs = l2_subs(p.n);
-  p.pre = g_scan_l2_pre;
-  const int smem = 3 * BLOCK * IT * (int)sizeof(T);
-  const void* fn = subs == 4 ? (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 4, 3>
-                             : (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 8, 3>;
-  return launch_l2_fn(fn, p, (int64_t)BLOCK * IT * subs, smem, device, s);
-}
-
-template <class T, class Op, int SUB>
-static int launch_scan_sub(ScanParams<typename WideAcc<T, Op>::type, const T*>& p, int64_t n, int device,
-                           cudaStream_t s) {
-  constexpr int ITEMS = ScanItems<T, Op>::value;
-  typedef ScanConfig<T, T, Op, BLOCK, ITEMS, SUB> C;
-  if (p.bulk_ok && g_scan_l2dyn && n >= (int64_t)g_scan_l2_min) return launch_scan_l2_any<PlainLoad<T>, Op>(p, device, s);
-  const int64_t nt64 = (n + C::TILE - 1) / C::TILE;
-  if (nt64 > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
-  p.ntiles = (u32)nt64;
-  auto k = scan_kernel<PlainLoad<T>, T, Op, BLOCK, ITEMS, SUB>;
-  if (C::SMEM > 48 * 1024) DRK_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  k<<<p.ntiles, BLOCK, C::SMEM, s>>>(p);
-  return 0;
-}
-
-template <class T, class Op>
-static int launch_scan(int exclusive, const T* in, T* out, int64_t n, const void* init_host, const void* carry_host,
-                       const void* carry_dev, void* seg_total, void* carry_out, void* scratch, size_t scratch_bytes,
-                       int device, void* stream) {
-  typedef typename WideAcc<T, Op>::type A;
-  const char* what = "drk_scan";
-  if (n < 1) return set_error(DRK_E_ARG, "drk_scan: n must be >= 1");
-  if (!in || !out) return set_error(DRK_E_ARG, "drk_scan: null in/out");
-  if (exclusive && !init_host) return set_error(DRK_E_ARG, "drk_scan: exclusive scan needs init");
-  if (carry_host && carry_dev) return set_error(DRK_E_ARG, "drk_scan: give at most one carry");
-  const size_t need_bytes = scan_scratch<T, Op>(n);
-  if (!scratch || scratch_bytes < need_bytes)
-    return set_error(DRK_E_SCRATCH, "drk_scan: scratch too small (need " + std::to_string(need_bytes) + ")");
-  if (int rc = prologue(device, what)) return rc;
-  char* b = (char*)scratch;
-  ScanParams<A, const T*> p;
-  memset(&p, 0, sizeof(p));
-  p.in = in;
-  p.out = out;
-  p.n = n;
-  p.exclusive = exclusive;
-  p.has_init = init_host != nullptr;
-  if (init_host) memcpy(&p.init, init_host, sizeof(A));
-  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
-  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
-  p.carry_ptr = (const A*)carry_dev;
-  p.seg_total = (A*)seg_total;
-  p.carry_out = (A*)carry_out;
-  p.counter = (u32*)b;
-  p.desc = (u64*)(b + 128);
-  p.t0slot = (u64*)(b + 64);
-  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;  // < 0: automatic (launch_l2_fn)
-  p.epoch = next_epoch(scratch);
-  p.bulk_ok = aligned16(in) && aligned16(out);
-  p.trace = (u64*)g_scan_trace;
-  p.debug = g_scan_debug;
-  cudaStream_t s = (cudaStream_t)stream;
-  int rc = 0;
-  switch (g_scan_sub) {
-    case 1: rc = launch_scan_sub<T, Op, 1>(p, n, device, s); break;
-    case 3: rc = launch_scan_sub<T, Op, 3>(p, n, device, s); break;
-    case 4: rc = launch_scan_sub<T, Op, 4>(p, n, device, s); break;
-    default: rc = launch_scan_sub<T, Op, 2>(p, n, device, s); break;
-  }
-  if (rc) return rc;
-  return epilogue(what);
-}
-
-template <class T>
-static int scan_op(int op, int exclusive, const T* in, T* out, int64_t n, const void* init_host,
-                   const void* carry_host, const void* carry_dev, void* seg_total, void* carry_out, void* scratch,
-                   size_t sb, int device, void* stream) {
-  switch (op) {
-    case DRK_ADD:
-      return launch_scan<T, OpAdd>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
-                                   scratch, sb, device, stream);
-    case DRK_MUL:
-      return launch_scan<T, OpMul>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
-                                   scratch, sb, device, stream);
-    case DRK_MIN:
-      return launch_scan<T, OpMin>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
-                                   scratch, sb, device, stream);
-    case DRK_MAX:
-      return launch_scan<T, OpMax>(exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total, carry_out,
-                                   scratch, sb, device, stream);
-  }
-  return set_error(DRK_E_ARG, "drk_scan: unknown op");
-}
-
-extern "C" size_t drk_scan_scratch_bytes(int dtype, int op, int64_t n) {
-  if (n < 1) n = 1;
-#define DRK_SS(T)                                               \
-  switch (op) {                                                 \
-    case DRK_ADD: return scan_scratch<T, OpAdd>(n);             \
-    case DRK_MUL: return scan_scratch<T, OpMul>(n);             \
-    case DRK_MIN: return scan_scratch<T, OpMin>(n);             \
-    case DRK_MAX: return scan_scratch<T, OpMax>(n);             \
-    default: return 0;                                          \
-  }
-  switch (dtype) {
-    case DRK_F32: DRK_SS(float)
-    case DRK_F64: DRK_SS(double)
-    case DRK_I32: DRK_SS(int)
-    case DRK_I64: DRK_SS(long long)
-  }
-#undef DRK_SS
-  return 0;
-}
-
-extern "C" int drk_scan(int dtype, int op, int exclusive, const void* in, void* out, int64_t n,
-                        const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total_dev,
-                        void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream) {
-  DRK_DISPATCH(dtype, "drk_scan", T, {
-    return scan_op<T>(op, exclusive, (const T*)in, (T*)out, n, init_host, carry_host, carry_dev, seg_total_dev,
-                      carry_out_dev, scratch, scratch_bytes, device, stream);
-  });
-}
-
-// ---------------------------------------------------------------------------------------
-// batched segments: one L2-scan launch over up to DRK_SCAN_SEGS buffers on one GPU (the
-// segments of a vector that share a device), so there is one ramp-up and one tail instead of
-// one per segment.  Each segment's look-back stays inside the segment; its carry comes from
-// the last tile of the segment before it (segdesc), as the driver's fold of the rounded
-// partials (algorithms.py:234-274), and its total is written straight to seg_totals[k].
-
-static size_t batch_tiles(int dtype, int nseg, const int64_t* ns) {
-  const int64_t tile = (int64_t)BLOCK * 8 * ((dtype == DRK_F64 || dtype == DRK_I64) ? 10 : 20);
-  size_t nt = 0;
-  for (int k = 0; k < nseg; ++k) nt += (size_t)((ns[k] + tile - 1) / tile);
-  return nt;
-}
-
-extern "C" size_t drk_scan_batch_scratch_bytes(int dtype, int op, int nseg, const int64_t* ns) {
-  (void)op;
-  return 128 + batch_tiles(dtype, nseg, ns) * 16 + (DRK_SCAN_SEGS + 1) * 16;
-}
-
-template <class T, class Op>
-static int launch_scan_batch(int exclusive, int nseg, const void* const* ins, void* const* outs, const int64_t* ns,
-                             const void* init_host, const void* carry_host, const void* carry_dev, void* seg_totals,
-                             void* carry_out, void* scratch, size_t scratch_bytes, int device, void* stream) {
-  typedef typename WideAcc<T, Op>::type A;
-  constexpr int IT = ScanItems<T, Op>::value;
-  constexpr int SUBS = 8;
-  constexpr int TILE = BLOCK * IT * SUBS;
-  const char* what = "drk_scan_batch";
-  if (nseg < 1 || nseg > DRK_SCAN_SEGS) return set_error(DRK_E_ARG, "drk_scan_batch: nseg out of range");
-  if (exclusive && !init_host) return set_error(DRK_E_ARG, "drk_scan_batch: exclusive scan needs init");
-  if (carry_host && carry_dev) return set_error(DRK_E_ARG, "drk_scan_batch: give at most one carry");
-  ScanParams<A, const T*> p;
-  memset(&p, 0, sizeof(p));
-  u64 nt = 0;
-  for (int k = 0; k < nseg; ++k) {
-    if (ns[k] < 1 || !ins[k] || !outs[k]) return set_error(DRK_E_ARG, "drk_scan_batch: empty or null segment");
-    if (!aligned16(ins[k]) || !aligned16(outs[k]))
-      return set_error(DRK_E_ARG, "drk_scan_batch: segments must be 16-byte aligned");
-    p.seg_first[k] = (u32)nt;
-    p.seg_in[k] = ins[k];
-    p.seg_out[k] = outs[k];
-    p.seg_n[k] = ns[k];
-    nt += (u64)((ns[k] + TILE - 1) / TILE);
-  }
-  p.seg_first[nseg] = (u32)nt;
-  if (nt > 0x7fffffffull) return set_error(DRK_E_ARG, "drk_scan_batch: too many tiles");
-  const size_t need = 128 + nt * 16 + (DRK_SCAN_SEGS + 1) * 16;
-  if (!scratch || scratch_bytes < need)
-    return set_error(DRK_E_SCRATCH, "drk_scan_batch: scratch too small (need " + std::to_string(need) + ")");
-  if (int rc = prologue(device, what)) return rc;
-  char* b = (char*)scratch;
-  p.nseg = nseg;
-  p.n = (int64_t)nt * TILE;  // tile count for the launcher (segments carry their own lengths)
-  p.exclusive = exclusive;
-  p.has_init = init_host != nullptr;
-  if (init_host) memcpy(&p.init, init_host, sizeof(A));
-  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
-  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
-  p.carry_ptr = (const A*)carry_dev;
-  p.seg_total = (A*)seg_totals;
-  p.carry_out = (A*)carry_out;
-  p.counter = (u32*)b;
-  p.desc = (u64*)(b + 128);
-  p.segdesc = (u64*)(b + 128 + nt * 16);
-  p.t0slot = (u64*)(b + 64);
-  p.epoch = next_epoch(scratch);
-  p.bulk_ok = 1;
-  p.pre = g_scan_l2_pre;
-  p.debug = g_scan_debug;
-  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;
-  const int smem = 3 * BLOCK * IT * (int)sizeof(T);
-  if (int rc = launch_l2_fn((const void*)scan_l2_kernel<PlainLoad<T>, Op, BLOCK, IT, SUBS, 3>, p, TILE, smem, device,
-                            (cudaStream_t)stream))
-    return rc;
-  return epilogue(what);
-}
-
-template <class T>
-static int scan_batch_op(int op, int exclusive, int nseg, const void* const* ins, void* const* outs, const int64_t* ns,
-                         const void* init_host, const void* carry_host, const void* carry_dev, void* seg_totals,
-                         void* carry_out, void* scratch, size_t sb, int device, void* stream) {
-  switch (op) {
-    case DRK_ADD:
-      return launch_scan_batch<T, OpAdd>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
-                                         carry_out, scratch, sb, device, stream);
-    case DRK_MUL:
-      return launch_scan_batch<T, OpMul>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
-                                         carry_out, scratch, sb, device, stream);
-    case DRK_MIN:
-      return launch_scan_batch<T, OpMin>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
-                                         carry_out, scratch, sb, device, stream);
-    case DRK_MAX:
-      return launch_scan_batch<T, OpMax>(exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals,
-                                         carry_out, scratch, sb, device, stream);
-  }
-  return set_error(DRK_E_ARG, "drk_scan_batch: unknown op");
-}
-
-extern "C" int drk_scan_batch(int dtype, int op, int exclusive, int nseg, const void* const* ins, void* const* outs,
-                              const int64_t* ns, const void* init_host, const void* carry_host, const void* carry_dev,
-                              void* seg_totals_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
-                              int device, void* stream) {
-  if (!ins || !outs || !ns) return set_error(DRK_E_ARG, "drk_scan_batch: null segment arrays");
-  DRK_DISPATCH(dtype, "drk_scan_batch", T, {
-    return scan_batch_op<T>(op, exclusive, nseg, ins, outs, ns, init_host, carry_host, carry_dev, seg_totals_dev,
-                            carry_out_dev, scratch, scratch_bytes, device, stream);
-  });
-}
-
-extern "C" int drk_scan_ex(int dtype, int op, int exclusive, int flags, const void* in, void* out, int64_t n,
-                           const void* init_host, const void* carry_host, const void* carry_dev,
-                           void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes, int device,
-                           void* stream) {
-  if (flags & ~DRK_SCAN_CHAINED) return set_error(DRK_E_ARG, "drk_scan_ex: unknown flags");
-  if ((flags & DRK_SCAN_CHAINED) && !carry_dev)
-    return set_error(DRK_E_ARG, "drk_scan_ex: a chained scan takes its carry from the previous scan (carry_dev)");
-  g_chain_launch = (flags & DRK_SCAN_CHAINED) != 0;
-  const int rc = drk_scan(dtype, op, exclusive, in, out, n, init_host, carry_host, carry_dev, seg_total_dev,
-                          carry_out_dev, scratch, scratch_bytes, device, stream);
-  g_chain_launch = 0;
-  return rc;
-}
-
-// ---------------------------------------------------------------------------------------
-// scans of fused views: inclusive_scan(transform(x, f), out) reads the leaves of the view and
-// writes only `out` (reference views.py:164-181 materialises f(x) first, algorithms.py:198-202
-// then scans it).  The loader (AOT ProdScanLoad / AffineScanLoad, or NVRTC-generated) gets
-// its leaf pointers and constants as JitWords.
-
-template <class A>
-static int fill_view_params(ScanParams<A, JitWords>& p, const uint64_t* words, int nwords, void* out, int64_t n,
-                            int exclusive, const void* init_host, const void* carry_host, const void* carry_dev,
-                            void* seg_total, void* carry_out, void* scratch, size_t scratch_bytes, size_t need,
-                            const char* what) {
-  if (n < 1) return set_error(DRK_E_ARG, std::string(what) + ": n must be >= 1");
-  if (!out || !words) return set_error(DRK_E_ARG, std::string(what) + ": null out/words");
-  if (nwords < 0 || nwords > DRK_JIT_WORDS)
-    return set_error(DRK_E_ARG, std::string(what) + ": at most " + std::to_string(DRK_JIT_WORDS) + " words");
-  if (exclusive && !init_host) return set_error(DRK_E_ARG, std::string(what) + ": exclusive scan needs init");
-  if (carry_host && carry_dev) return set_error(DRK_E_ARG, std::string(what) + ": give at most one carry");
-  if (!scratch || scratch_bytes < need)
-    return set_error(DRK_E_SCRATCH, std::string(what) + ": scratch too small (need " + std::to_string(need) + ")");
-  memset(&p, 0, sizeof(p));
-  memcpy(p.in.w, words, sizeof(uint64_t) * nwords);
-  p.out = out;
-  p.n = n;
-  p.exclusive = exclusive;
-  p.has_init = init_host != nullptr;
-  if (init_host) memcpy(&p.init, init_host, sizeof(A));
-  p.carry_kind = carry_host ? 1 : (carry_dev ? 2 : 0);
-  if (carry_host) memcpy(&p.carry_val, carry_host, sizeof(A));
-  p.carry_ptr = (const A*)carry_dev;
-  p.seg_total = (A*)seg_total;
-  p.carry_out = (A*)carry_out;
-  char* b = (char*)scratch;
-  p.counter = (u32*)b;
-  p.t0slot = (u64*)(b + 64);
-  p.desc = (u64*)(b + 128);
-  p.epoch = next_epoch(scratch);
-  p.stagger_ns = g_scan_stagger > 0 ? (u32)g_scan_stagger : 0;
-  p.trace = (u64*)g_scan_trace;
-  p.debug = g_scan_debug;
-  return 0;
-}
-
-// One fused-view scan: the L2 kernel (l2_4 / l2_8 by size) when every leaf is vector-aligned
-// (vec_ok) and out is 16-byte aligned, else the single-pass kernel `one` (3 sub-tiles).
-template <class A>
-static int launch_view_scan(const void* l2_4, const void* l2_8, const void* one, int v_bytes,
-                            ScanParams<A, JitWords>& p, int vec_ok, int device, cudaStream_t s) {
-  const int items = v_bytes == 4 ? 20 : 10;
-  if (vec_ok && aligned16(p.out) && g_scan_l2dyn && p.n >= (int64_t)g_scan_l2_min) {
-    p.bulk_ok = 1;
-    p.pre = g_scan_l2_pre;
-    const int subs = l2_subs(p.n);
-    return launch_l2_fn(subs == 4 ? l2_4 : l2_8, p, (int64_t)BLOCK * items * subs, 3 * BLOCK * items * v_bytes, device,
-                        s);
-  }
-  constexpr int SUB = 3;
-  const int64_t tile = (int64_t)BLOCK * items * SUB;
-  const int64_t nt = (p.n + tile - 1) / tile;
-  if (nt > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan_view: too many tiles");
-  p.ntiles = (u32)nt;
-  p.bulk_ok = 0;
-  const int smem = (int)tile * v_bytes;
-  DRK_CHECK(cudaFuncSetAttribute(one, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)nt);
-  cfg.blockDim = dim3(BLOCK);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  void* args[] = {&p};
-  DRK_CHECK(cudaLaunchKernelExC(&cfg, one, args));
-  return 0;
-}
-
-template <class LDR, class Op>
-static int view_scan_aot(const uint64_t* words, int nwords, int vec_ok, int exclusive, void* out, int64_t n,
-                         const void* init_host, const void* carry_host, const void* carry_dev, void* seg_total,
-                         void* carry_out, void* scratch, size_t scratch_bytes, int device, void* stream) {
-  typedef typename LDR::V T;
-  typedef typename WideAcc<T, Op>::type A;
-  constexpr int IT = ScanItems<T, Op>::value;
-  const char* what = "drk_scan_view";
-  ScanParams<A, JitWords> p;
-  if (int rc = fill_view_params(p, words, nwords, out, n, exclusive, init_host, carry_host, carry_dev, seg_total,
-                                carry_out, scratch, scratch_bytes, scan_scratch<T, Op>(n), what))
-    return rc;
-  if (int rc = prologue(device, what)) return rc;
-  if (int rc = launch_view_scan(
-          (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 4, 3>, (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 8, 3>,
-          (const void*)scan_kernel<LDR, T, Op, BLOCK, IT, 3>, (int)sizeof(T), p, vec_ok, device, (cudaStream_t)stream))
-    return rc;
-  return epilogue(what);
-}
-
-extern "C" int drk_scan_view(int kind, int dtype, int op, int exclusive, const uint64_t* words, int nwords,
-                             int vec_ok, void* out, int64_t n, const void* init_host, const void* carry_host,
-                             const void* carry_dev, void* seg_total_dev, void* carry_out_dev, void* scratch,
-                             size_t scratch_bytes, int device, void* stream) {
-  if (op != DRK_ADD) return set_error(DRK_E_ARG, "drk_scan_view: the AOT view scans take op = DRK_ADD");
-  if (kind != DRK_VIEW_PRODUCT && kind != DRK_VIEW_AFFINE) return set_error(DRK_E_ARG, "drk_scan_view: unknown kind");
-  DRK_DISPATCH(dtype, "drk_scan_view", T, {
-    if (kind == DRK_VIEW_PRODUCT)
-      return view_scan_aot<ProdScanLoad<T>, OpAdd>(words, nwords, vec_ok, exclusive, out, n, init_host, carry_host,
-                                                    carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes,
-                                                    device, stream);
-    return view_scan_aot<AffineScanLoad<T>, OpAdd>(words, nwords, vec_ok, exclusive, out, n, init_host, carry_host,
-                                                    carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes,
-                                                    device, stream);
-  });
-}
-
-extern "C" int drk_scan_view_ex(int kind, int dtype, int op, int exclusive, int flags, const uint64_t* words,
-                                int nwords, int vec_ok, void* out, int64_t n, const void* init_host,
-                                const void* carry_host, const void* carry_dev, void* seg_total_dev,
-                                void* carry_out_dev, void* scratch, size_t scratch_bytes, int device, void* stream) {
-  if (flags & ~DRK_SCAN_CHAINED) return set_error(DRK_E_ARG, "drk_scan_view_ex: unknown flags");
-  if ((flags & DRK_SCAN_CHAINED) && !carry_dev)
-    return set_error(DRK_E_ARG, "drk_scan_view_ex: a chained scan takes its carry from the previous scan");
-  g_chain_launch = (flags & DRK_SCAN_CHAINED) != 0;
-  const int rc = drk_scan_view(kind, dtype, op, exclusive, words, nwords, vec_ok, out, n, init_host, carry_host,
-                               carry_dev, seg_total_dev, carry_out_dev, scratch, scratch_bytes, device, stream);
-  g_chain_launch = 0;
-  return rc;
-}
-
-// NVRTC view scans: the module defines drk_scan_l2_4 / drk_scan_l2_8 (scan_l2_body) and
-// drk_scan_1p (scan_kernel_body, 3 sub-tiles) over its generated loader.
-extern "C" int drk_get_jit_kernel(void* handle, const char* kernel, const void** fn);
-
-extern "C" int drk_jit_scan_view(void* handle, int v_bytes, int acc_bytes, int exclusive, int flags,
-                                 const uint64_t* words, int nwords, int vec_ok, void* out, int64_t n,
-                                 const void* init_host, const void* carry_host, const void* carry_dev,
-                                 void* seg_total_dev, void* carry_out_dev, void* scratch, size_t scratch_bytes,
-                                 int device, void* stream) {
-  const char* what = "drk_jit_scan_view";
-  if (v_bytes != 4 && v_bytes != 8) return set_error(DRK_E_ARG, "drk_jit_scan_view: v_bytes must be 4 or 8");
-  if (flags & ~DRK_SCAN_CHAINED) return set_error(DRK_E_ARG, "drk_jit_scan_view: unknown flags");
-  const void *k4 = nullptr, *k8 = nullptr, *k1 = nullptr;
-  if (int rc = drk_get_jit_kernel(handle, "drk_scan_l2_4", &k4)) return set_error(rc, "drk_jit_scan_view: no kernel");
-  if (int rc = drk_get_jit_kernel(handle, "drk_scan_l2_8", &k8)) return set_error(rc, "drk_jit_scan_view: no kernel");
-  if (int rc = drk_get_jit_kernel(handle, "drk_scan_1p", &k1)) return set_error(rc, "drk_jit_scan_view: no kernel");
-  const size_t need = 128 + (size_t)((n + BLOCK * (v_bytes == 4 ? 20 : 10) - 1) / (BLOCK * (v_bytes == 4 ? 20 : 10))) * 16;
-  if (int rc = prologue(device, what)) return rc;
-  g_chain_launch = (flags & DRK_SCAN_CHAINED) != 0;
-  int rc = 0;
-  if (acc_bytes == 8) {
-    ScanParams<double, JitWords> p;
-    rc = fill_view_params(p, words, nwords, out, n, exclusive, init_host, carry_host, carry_dev, seg_total_dev,
-                          carry_out_dev, scratch, scratch_bytes, need, what);
-    if (!rc) rc = launch_view_scan(k4, k8, k1, v_bytes, p, vec_ok, device, (cudaStream_t)stream);
-  } else if (acc_bytes == 4) {
-    ScanParams<float, JitWords> p;
-    rc = fill_view_params(p, words, nwords, out, n, exclusive, init_host, carry_host, carry_dev, seg_total_dev,
-                          carry_out_dev, scratch, scratch_bytes, need, what);
-    if (!rc) rc = launch_view_scan(k4, k8, k1, v_bytes, p, vec_ok, device, (cudaStream_t)stream);
-  } else {
-    rc = set_error(DRK_E_ARG, "drk_jit_scan_view: acc_bytes must be 4 or 8");
-  }
-  g_chain_launch = 0;
-  if (rc) return rc;
-  return epilogue(what);
 }
 
 // ---------------------------------------------------------------------------------------

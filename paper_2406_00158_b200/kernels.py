@@ -447,12 +447,12 @@ def run_scan_view(T, opcode, exclusive, view: ScanView, out_ptr, n, lctx: Launch
         return
     from . import codegen
 
-    mod, words, items = codegen.scan_view_plan(view, T, opcode, combiner)
+    mod, words, geom = codegen.scan_view_plan(view, T, opcode, combiner)
     wbuf = _keep(lctx, (ctypes.c_uint64 * len(words))(*[w & 0xFFFFFFFFFFFFFFFF for w in words]))
-    nbytes = int(_lib.load().drk_jit_scan_scratch_bytes(n, 256 * items))
+    nbytes = int(_lib.load().drk_jit_scan_scratch_bytes(n, 256 * geom[4]))
     scratch = st.scan_scratch(nbytes, scratch_index)
-    args = (mod.handle, T.itemsize, A.itemsize, *tail, flags, wbuf, len(words), 1 if view.vec_ok() else 0, *common,
-            scratch.data_ptr(), scratch.numel(), st.index, st.handle)
+    args = (mod.handle, T.itemsize, A.itemsize, *geom, *tail, flags, wbuf, len(words), 1 if view.vec_ok() else 0,
+            *common, scratch.data_ptr(), scratch.numel(), st.index, st.handle)
     if _PROFILE is None:
         _lib.call("drk_jit_scan_view", *args)
         return

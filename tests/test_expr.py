@@ -204,17 +204,26 @@ def _scan_view_source(monkeypatch, node, leaves, T, opcode, combiner=None):
     monkeypatch.setattr(codegen, "compile_module", fake_compile)
     codegen._SCAN_VIEW_PLANS.clear()
     view = kernels.ScanView(node, leaves, [0] * len(leaves), 100)
-    mod, words, items = codegen.scan_view_plan(view, T, opcode, combiner)
-    return got["src"], words, items
+    mod, words, geom = codegen.scan_view_plan(view, T, opcode, combiner)
+    return got["src"], words, geom
 
 
 @pytest.mark.parametrize("T", [np.float32, np.int64])
 def test_scan_view_nvrtc_compiles(meta_rt, monkeypatch, T):
     lw = _lowered(meta_rt, [T, np.float64])
     node = expr.cast(expr.trace(lambda t: np.sqrt(t[0] * t[1] + 1.5) * 2, lw.value), T)
-    src, words, items = _scan_view_source(monkeypatch, node, lw.leaves, np.dtype(T), 0)
-    assert "drk_scan_l2_8" in src and "drk_scan_1p" in src
-    assert len(words) <= 16 and items == (20 if np.dtype(T).itemsize == 4 else 10)
+    src, words, geom = _scan_view_source(monkeypatch, node, lw.leaves, np.dtype(T), 0)
+    assert "drk_scan_l2_l" in src and "drk_scan_1p" in src
+    same = np.dtype(T).itemsize == 8  # the float64 leaf is staged with a same-size value only
+    assert len(words) <= 16 and geom[1] == (2 if same else 0)
+    assert len(codegen.cubin_for(src, "scan_view.cu")) > 1000
+
+
+def test_scan_view_nvrtc_staged_single_leaf(meta_rt, monkeypatch):
+    lw = _lowered(meta_rt, [np.float32, np.float32])
+    node = expr.trace(lambda t: np.where(t[0] > 0.5, t[0] * 3.0, -t[0]).astype(np.float32), lw.value)
+    src, words, geom = _scan_view_source(monkeypatch, node, lw.leaves, np.dtype(np.float32), 0)
+    assert geom == (20, 1, 4, 8, 20) and "compute" in src
     assert len(codegen.cubin_for(src, "scan_view.cu")) > 1000
 
 
