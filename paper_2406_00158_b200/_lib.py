@@ -163,9 +163,17 @@ def check(rc: int, func: str) -> None:
         raise DrkError(rc, func, msg.decode(errors="replace"))
 
 
+_FUNCS = {}
+
+
 def call(name: str, *args) -> None:
     """Call an int-returning entry point and raise DrkError on failure."""
-    check(getattr(load(), name)(*args), name)
+    fn = _FUNCS.get(name)
+    if fn is None:
+        fn = _FUNCS[name] = getattr(load(), name)
+    rc = fn(*args)
+    if rc != 0:
+        check(rc, name)
 
 
 def device_count() -> int:

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib, expr, kernels
+from . import _lib, expr, kernels, plans
 from . import views as _views
 from .containers import DistributedVector
 from .core import has_segments, is_aligned, runtime_of, segments_of
@@ -133,30 +133,37 @@ def _promote_python(value):
 def for_each(r, fn, vectorized: bool = False) -> None:
     """Apply fn to every element; its non-None result replaces the element (a tuple for
     zips, None components skipped).  Effects are visible on return (algorithms.py:86-98)."""
-    pieces = _pieces(r)
-    if not pieces:
-        return
-    rt = _require_runtime(runtime_of(r), "for_each")
-    cache = {}
+    fk = expr._fn_key(fn)
+    key, dvs, plan = plans.lookup("for_each", r, (fk, vectorized)) if fk is not None else (None, None, None)
+    if plan is None:
+        pieces = _pieces(r)
+        if not pieces:
+            return
+        rt = _require_runtime(runtime_of(r), "for_each")
+        cache = {}
+        work = []
+        for piece in pieces:
+            lw = lower(piece)
+            value = lw.value if vectorized else _promote_python(lw.value)
+            vkey = _views._value_key(value)
+            if vkey not in cache:
+                cache[vkey] = expr.trace_cached(fn, value, vkey)
+            result = cache[vkey]
+            if result is None:
+                raise TypeError(
+                    "for_each function returned None for every element: it only has side effects, which "
+                    "cannot run inside a device kernel"
+                )
+            writes = []
+            _collect_writes(result, lw.target, writes)
+            if writes:
+                work.append((rt.state_of(writes[0][0].handle.locale), writes, lw.leaves, lw.length))
+        plan = plans.store(key, dvs, (rt, work))
+    rt, work = plan
     launches = []
-    for piece in pieces:
-        lw = lower(piece)
-        value = lw.value if vectorized else _promote_python(lw.value)
-        key = _views._value_key(value)
-        if key not in cache:
-            cache[key] = expr.trace_cached(fn, value, key)
-        result = cache[key]
-        if result is None:
-            raise TypeError(
-                "for_each function returned None for every element: it only has side effects, which "
-                "cannot run inside a device kernel"
-            )
-        writes = []
-        _collect_writes(result, lw.target, writes)
-        if not writes:
-            continue
-        launch = _launch_for(rt, writes[0][0].handle.locale)
-        run_map(writes, lw.leaves, lw.length, launch)
+    for st, writes, leaves, length in work:
+        launch = Launch(st)
+        run_map(writes, leaves, length, launch)
         launches.append(launch)
     _finish(rt, launches)
 
@@ -217,70 +224,120 @@ def _partial_dtype(op: BinaryOp, dtype):
 def reduce(r, init=0, op=add):
     """Fold all elements onto init: per-segment device partials, then an ascending fold on
     the driver (algorithms.py:135-150), so exact types give identical results for every
-    segment count."""
+    segment count.  The lowered plan of r is memoised by r's structure (plans.py)."""
     op = as_binary_op(op)
-    pieces = _pieces(r)
-    if not pieces:
-        return init.item() if isinstance(init, np.generic) else init
-    rt = _require_runtime(runtime_of(r), "reduce")
-    partials = _segment_partials(rt, pieces, op)
+    opk = _op_key(op)
+    key, dvs, plan = plans.lookup("reduce", r, opk) if opk is not None else (None, None, None)
+    if plan is None:
+        pieces = _pieces(r)
+        if not pieces:
+            return init.item() if isinstance(init, np.generic) else init
+        plan = plans.store(key, dvs, _ReducePlan(_require_runtime(runtime_of(r), "reduce"), pieces, op))
+    partials = plan.run()
     acc = init
     for p in partials:
         acc = op.fn(acc, p)
     return acc.item() if isinstance(acc, np.generic) else acc
 
 
-def _segment_partials(rt, pieces, op):
-    opcode = _opcode(op)
-    lowered = []
-    for piece in pieces:
-        lw = lower(piece)
-        if isinstance(lw.value, tuple):
-            raise TypeError("reduce needs scalar elements; apply a transform to the zip first")
-        lowered.append(lw)
-    combiner = None
-    if opcode is None:
-        combiner = op  # traced by codegen per value dtype
-    need = {}
-    for lw in lowered:
-        st = rt.state_of(lw.rank if lw.rank is not None else 0)
-        need[id(st)] = (st, need.get(id(st), (st, 0))[1] + 1)
-    for st, k in need.values():
-        st.ensure_results(k)  # before any launch: growing the slot buffer reallocates it
-    slots = {}
-    order = []
-    launches = {}
-    batched = _batch_reduce(rt, lowered, opcode) if opcode is not None else None
-    if batched is not None:
-        order, launches, slots = batched
-    for lw in lowered if batched is None else ():
-        st = rt.state_of(lw.rank if lw.rank is not None else 0)
-        launch = launches.setdefault(id(st), Launch(st))
-        slot = slots.get(id(st), 0)
-        slots[id(st)] = slot + 1
-        node = lw.value if opcode is not None else _promote_python(lw.value)
-        run_reduce(node, lw.leaves, lw.length, opcode, combiner, launch, slot)
-        order.append((st, slot, node.dtype))
-    raw = {id(l.state): l.state.fetch_host_results(slots[id(l.state)]) for l in launches.values()}
-    out = []
-    for st, slot, vdt in order:
-        if opcode is not None:
-            A = _lib.acc_dtype(vdt, opcode)
-            a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + A.itemsize].tobytes(), dtype=A)[0]
-            out.append(a.astype(_partial_dtype(op, vdt)))
+def _op_key(op: BinaryOp):
+    """Cache identity of a binary operator: the ufunc and the function (by behaviour for
+    traced Python functions), or None if the function can reach mutable state."""
+    fn = op.fn
+    if isinstance(fn, (type(min), type(operator.add))) or fn in (min, max):
+        fk = ("builtin", fn)
+    else:
+        fk = expr._fn_key(fn)
+        if fk is None:
+            return None
+    return (getattr(op.ufunc, "__name__", None), fk)
+
+
+class _ReducePlan:
+    """A reduce over fixed segments: lowered pieces, their launch plan (one batched launch when
+    a single GPU holds every piece and the catalogue covers them), and the result decoding."""
+
+    __slots__ = ("rt", "lowered", "op", "opcode", "combiner", "batch", "order", "need")
+
+    def __init__(self, rt, pieces, op):
+        self.rt = rt
+        self.op = op
+        self.opcode = _opcode(op)
+        self.combiner = op if self.opcode is None else None
+        lowered = []
+        for piece in pieces:
+            lw = lower(piece)
+            if isinstance(lw.value, tuple):
+                raise TypeError("reduce needs scalar elements; apply a transform to the zip first")
+            lowered.append(lw)
+        self.lowered = lowered
+        need = {}
+        for lw in lowered:
+            st = rt.state_of(lw.rank if lw.rank is not None else 0)
+            need[id(st)] = (st, need.get(id(st), (st, 0))[1] + 1)
+        self.need = list(need.values())
+        self.batch = _batch_reduce_plan(rt, lowered, self.opcode) if self.opcode is not None else None
+
+    def run(self):
+        for st, k in self.need:
+            st.ensure_results(k)  # before any launch: growing the slot buffer reallocates it
+        if self.batch is not None:
+            order, launches, slots = self.batch.launch()
         else:
-            a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + vdt.itemsize].tobytes(), dtype=vdt)[0]
-            out.append(a.item())
-    return out
+            order, launches, slots = [], {}, {}
+            for lw in self.lowered:
+                st = self.rt.state_of(lw.rank if lw.rank is not None else 0)
+                launch = launches.setdefault(id(st), Launch(st))
+                slot = slots.get(id(st), 0)
+                slots[id(st)] = slot + 1
+                node = lw.value if self.opcode is not None else _promote_python(lw.value)
+                run_reduce(node, lw.leaves, lw.length, self.opcode, self.combiner, launch, slot)
+                order.append((st, slot, node.dtype))
+        raw = {id(l.state): l.state.fetch_host_results(slots[id(l.state)]) for l in launches.values()}
+        out = []
+        op = self.op
+        for st, slot, vdt in order:
+            if self.opcode is not None:
+                A = _lib.acc_dtype(vdt, self.opcode)
+                a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + A.itemsize].tobytes(), dtype=A)[0]
+                out.append(a.astype(_partial_dtype(op, vdt)))
+            else:
+                a = np.frombuffer(raw[id(st)][slot * 8 : slot * 8 + vdt.itemsize].tobytes(), dtype=vdt)[0]
+                out.append(a.item())
+        return out
 
 
-def _batch_reduce(rt, lowered, opcode):
+def _segment_partials(rt, pieces, op):
+    return _ReducePlan(rt, pieces, op).run()
+
+
+class _BatchReduce:
     """Several segments on one GPU, each a catalogue reduction (a plain device array, or the
-    product of two for dot): one drk_reduce_batch / drk_dot_batch launch instead of one
-    launch per segment.  Returns (order, launches, slots) like the per-segment loop, or None
-    when the pieces do not qualify."""
-    from .runtime import await_pending
+    product of two for dot): one drk_reduce_batch / drk_dot_batch launch, its argument arrays
+    built once."""
 
+    __slots__ = ("st", "kind", "code", "opcode", "m", "xs", "ys", "ns", "handles", "dtypes", "total")
+
+    def launch(self):
+        from .runtime import await_pending
+
+        st = self.st
+        await_pending(st, self.handles)
+        launch = Launch(st)
+        scratch = st.reduce_batch_scratch(self.m)
+        if self.kind == "reduce":
+            kernels.launch_kernel("drk_reduce_batch", launch, self.total, self.code, self.opcode, self.m, self.xs,
+                                  self.ns, st.host_result_dev_ptr(0), scratch.data_ptr())
+        else:
+            kernels.launch_kernel("drk_dot_batch", launch, self.total, self.code, self.m, self.xs, self.ys, self.ns,
+                                  st.host_result_dev_ptr(0), scratch.data_ptr())
+        order = [(st, j, dt) for j, dt in enumerate(self.dtypes)]
+        return order, {id(st): launch}, {id(st): self.m}
+
+
+def _batch_reduce_plan(rt, lowered, opcode):
+    """A _BatchReduce for the pieces, or None when they do not qualify (one piece, several
+    GPUs, or an expression outside the catalogue)."""
     m = len(lowered)
     if not 1 < m <= _lib.RED_SEGS:
         return None
@@ -288,24 +345,21 @@ def _batch_reduce(rt, lowered, opcode):
     if len(states) != 1:
         return None
     st = rt.state_of(lowered[0].rank if lowered[0].rank is not None else 0)
-    plans = [kernels.catalogue_reduce(lw.value, lw.leaves, opcode, st.index) for lw in lowered]
-    if any(p is None for p in plans) or len({(p[0], p[1]) for p in plans}) != 1:
+    plans_ = [kernels.catalogue_reduce(lw.value, lw.leaves, opcode, st.index) for lw in lowered]
+    if any(p is None for p in plans_) or len({(p[0], p[1]) for p in plans_}) != 1:
         return None
-    kind, code = plans[0][0], plans[0][1]
-    await_pending(st, [lf.handle for lw in lowered for lf in lw.leaves if lf.handle is not None])
-    launch = Launch(st)
-    ns = (ctypes.c_int64 * m)(*[lw.length for lw in lowered])
-    xs = (ctypes.c_void_p * m)(*[p[2] for p in plans])
-    scratch = st.reduce_batch_scratch(m)
-    if kind == "reduce":
-        kernels.launch_kernel("drk_reduce_batch", launch, sum(ns), code, opcode, m, xs, ns,
-                              st.host_result_dev_ptr(0), scratch.data_ptr())
-    else:
-        ys = (ctypes.c_void_p * m)(*[p[3] for p in plans])
-        kernels.launch_kernel("drk_dot_batch", launch, sum(ns), code, m, xs, ys, ns,
-                              st.host_result_dev_ptr(0), scratch.data_ptr())
-    order = [(st, j, lw.value.dtype) for j, lw in enumerate(lowered)]
-    return order, {id(st): launch}, {id(st): m}
+    b = _BatchReduce()
+    b.st = st
+    b.kind, b.code = plans_[0][0], plans_[0][1]
+    b.opcode = opcode
+    b.m = m
+    b.ns = (ctypes.c_int64 * m)(*[lw.length for lw in lowered])
+    b.total = sum(lw.length for lw in lowered)
+    b.xs = (ctypes.c_void_p * m)(*[p[2] for p in plans_])
+    b.ys = (ctypes.c_void_p * m)(*[p[3] for p in plans_]) if b.kind == "dot" else None
+    b.handles = [lf.handle for lw in lowered for lf in lw.leaves if lf.handle is not None]
+    b.dtypes = [lw.value.dtype for lw in lowered]
+    return b
 
 
 # ----------------------------------------------------------------------------------------
@@ -330,7 +384,7 @@ def _scan_entry(r, out, op, exclusive, init):
     r_seg, o_seg = has_segments(r), has_segments(out)
     if not o_seg:
         raise TypeError("scan output must be a segmented device range")
-    if r is out or (r_seg and is_aligned(r, out)):
+    if r is out or (r_seg and _aligned(r, out)):
         _scan_impl(r, out, op, exclusive, init, want_partials=False)
         return
     if not isinstance(out, DistributedVector):
@@ -338,6 +392,23 @@ def _scan_entry(r, out, op, exclusive, init):
     temp = DistributedVector.like_distribution(out.runtime, out.distribution, out.dtype)
     copy(r, temp)
     _scan_impl(temp, out, op, exclusive, init, want_partials=False)
+
+
+def _aligned(r, out) -> bool:
+    """core.is_aligned, memoised by the structure of both ranges (plans.py)."""
+    key = None
+    if plans._ENABLED:
+        dvs = []
+        kr, ko = plans.view_key(r, dvs), plans.view_key(out, dvs)
+        if kr is not None and ko is not None:
+            key = ("aligned", kr, ko)
+            hit = plans.CACHE.get(key)
+            if hit is not None:
+                return hit[0]
+    value = is_aligned(r, out)
+    if key is not None:
+        plans.CACHE.put(key, dvs, (value,))
+    return value
 
 
 def _scan_aligned(r, out, op, exclusive, init) -> list:
@@ -360,30 +431,28 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
     the host does not wait for the totals, later work on the stream is ordered after it,
     and kernels on other GPUs that read its output wait for it (kernels.stage_leaves)."""
     op = as_binary_op(op)
-    in_segs = segments_of(r)
-    out_segs = segments_of(out)
-    live = [k for k, s in enumerate(in_segs) if len(s)]
-    partials = [None] * len(in_segs)
-    if not live:
-        return partials
-    rt = _require_runtime(runtime_of(out, r), "scan")
     opcode = _opcode(op)
     if opcode is None:
         from . import codegen
 
+        in_segs = segments_of(r)
+        out_segs = segments_of(out)
+        live = [k for k, s in enumerate(in_segs) if len(s)]
+        if not live:
+            return [None] * len(in_segs)
+        rt = _require_runtime(runtime_of(out, r), "scan")
         return codegen.custom_scan(rt, in_segs, out_segs, live, op, exclusive, init, carry)
+    rt, nseg, live, lowered = _scan_lowered(r, out)
+    partials = [None] * nseg
+    if not live:
+        return partials
 
     # 1. what each live segment scan reads: a plain device array in the output dtype, or a
     #    view — fused into the scan kernel (its leaves are read, nothing is materialised;
     #    the reference materialises f's result, views.py:164-181, then accumulates it)
     work = []
     launches = {}
-    for k in live:
-        lw = lower(in_segs[k])
-        tgt = lower(out_segs[k]).target
-        if not isinstance(tgt, Target):
-            raise TypeError("scan output segments must be writable vector storage")
-        st = rt.state_of(out_segs[k].rank)
+    for k, lw, tgt, st in lowered:
         launch = launches.setdefault(id(st), Launch(st))
         node = lw.value
         if isinstance(node, tuple):
@@ -600,6 +669,38 @@ def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, ini
     return partials
 
 
+def _scan_lowered(r, out):
+    """(runtime, segment count, live segment indices, [(k, lowered input, output Target,
+    device state)]) of an aligned scan r -> out, memoised by the structure of both
+    (plans.py); device state (pending transfers, staging) is resolved per call."""
+    key = None
+    if plans._ENABLED:
+        dvs = []
+        kr, ko = plans.view_key(r, dvs), plans.view_key(out, dvs)
+        if kr is not None and ko is not None:
+            key = ("scan", kr, ko)
+            hit = plans.CACHE.get(key)
+            if hit is not None:
+                return hit
+    in_segs = segments_of(r)
+    out_segs = segments_of(out)
+    live = [k for k, s in enumerate(in_segs) if len(s)]
+    if not live:
+        return None, len(in_segs), live, []
+    rt = _require_runtime(runtime_of(out, r), "scan")
+    lowered = []
+    for k in live:
+        lw = lower(in_segs[k])
+        tgt = lower(out_segs[k]).target
+        if not isinstance(tgt, Target):
+            raise TypeError("scan output segments must be writable vector storage")
+        lowered.append((k, lw, tgt, rt.state_of(out_segs[k].rank)))
+    value = (rt, len(in_segs), live, lowered)
+    if key is not None:
+        plans.CACHE.put(key, dvs, value)
+    return value
+
+
 # Views scanned in a fused kernel (kernels.run_scan_view); False materialises them first.
 _FUSE_SCAN_VIEWS = True
 
@@ -811,28 +912,46 @@ def copy(src, dst) -> None:
         raise ValueError(f"copy length mismatch: source {len(src)}, destination {len(dst)}")
     if len(src) == 0:
         return
-    rt = runtime_of(dst, src)
-    s_seg, d_seg = has_segments(src), has_segments(dst)
-    if s_seg and d_seg and is_aligned(src, dst):
-        pairs = [(s, d) for s, d in zip(segments_of(src), segments_of(dst)) if len(s)]
-    else:
-        src_list = segments_of(src) if s_seg else [_views._as_piece(src, len(src))]
-        dst_list = segments_of(dst) if d_seg else [_views._as_piece(dst, len(dst))]
-        pairs = [tuple(ch.components) for ch in _views.realign_segments([src_list, dst_list])]
-    rt = _require_runtime(rt, "copy")
+    key = None
+    if plans._ENABLED:
+        dvs = []
+        ks, kd = plans.view_key(src, dvs), plans.view_key(dst, dvs)
+        if ks is not None and kd is not None:
+            key = ("copy", ks, kd)
+    plan = plans.CACHE.get(key) if key is not None else None
+    if plan is None:
+        rt = runtime_of(dst, src)
+        s_seg, d_seg = has_segments(src), has_segments(dst)
+        if s_seg and d_seg and is_aligned(src, dst):
+            pairs = [(s, d) for s, d in zip(segments_of(src), segments_of(dst)) if len(s)]
+        else:
+            src_list = segments_of(src) if s_seg else [_views._as_piece(src, len(src))]
+            dst_list = segments_of(dst) if d_seg else [_views._as_piece(dst, len(dst))]
+            pairs = [tuple(ch.components) for ch in _views.realign_segments([src_list, dst_list])]
+        rt = _require_runtime(rt, "copy")
+        work = []
+        for s, d in pairs:
+            ls = lower(s)
+            if isinstance(ls.value, tuple):
+                raise TypeError("copy source elements must be scalars")
+            if isinstance(d, _views.LocalPiece):
+                work.append((ls, d, None))
+                continue
+            tgt = lower(d).target
+            if isinstance(tgt, ReadOnly):
+                raise TypeError(f"cannot write through read-only {tgt.what}")
+            work.append((ls, tgt, rt.state_of(d.rank)))
+        plan = (rt, work)
+        if key is not None:
+            plans.CACHE.put(key, dvs, plan)
+    rt, work = plan
     launches = []
-    for s, d in pairs:
-        ls = lower(s)
-        if isinstance(ls.value, tuple):
-            raise TypeError("copy source elements must be scalars")
-        if isinstance(d, _views.LocalPiece):
+    for ls, d, st in work:
+        if st is None:
             _copy_to_host(rt, ls, d, launches)
             continue
-        tgt = lower(d).target
-        if isinstance(tgt, ReadOnly):
-            raise TypeError(f"cannot write through read-only {tgt.what}")
-        launch = Launch(rt.state_of(d.rank))
-        run_map([(tgt, ls.value)], ls.leaves, ls.length, launch)
+        launch = Launch(st)
+        run_map([(d, ls.value)], ls.leaves, ls.length, launch)
         launches.append(launch)
     _finish(rt, launches)
 

@@ -527,13 +527,26 @@ def functools_partial():
     return functools.partial
 
 
+_CODE = type(_freeze.__code__)
+
+
+def _all_names(code, out):
+    """Names a code object and the code objects nested in it (inner lambdas, comprehensions)
+    may look up as globals."""
+    out.update(code.co_names)
+    for c in code.co_consts:
+        if type(c) is _CODE:
+            _all_names(c, out)
+    return out
+
+
 def _fn_key_strict(fn, depth=0):
     code = getattr(fn, "__code__", None)
     if code is None:
         raise _Uncacheable("no code")
     cells = tuple(_freeze(c.cell_contents, depth) for c in (fn.__closure__ or ()))
     g = fn.__globals__
-    glob = tuple((nm, _freeze(g[nm], depth)) for nm in code.co_names if nm in g)
+    glob = tuple((nm, _freeze(g[nm], depth)) for nm in sorted(_all_names(code, set())) if nm in g)
     defaults = _freeze(tuple(fn.__defaults__ or ()), depth)
     kwdefaults = _freeze(tuple(sorted((fn.__kwdefaults__ or {}).items())), depth)
     return (code, defaults, kwdefaults, cells, glob)
@@ -545,6 +558,10 @@ def _fn_key(fn):
     recursively).  None — no caching, the function is traced on every call like the
     reference calls it every time — when it can reach mutable state (an object attribute,
     a list, an array, a user module) whose value could change between calls."""
+    code = getattr(fn, "__code__", None)
+    if (code is not None and not code.co_names and fn.__closure__ is None and fn.__defaults__ is None
+            and not fn.__kwdefaults__ and not any(type(c) is _CODE for c in code.co_consts)):
+        return (code,)  # a pure function of its argument (lambda t: t[0] * t[1]): the code alone
     if isinstance(fn, functools_partial()):
         try:
             return ("partial", _freeze(fn, 0))

@@ -151,6 +151,7 @@ class DeviceState:
         with t.cuda.stream(self.stream):
             self._results = t.zeros(slots * self.RESULT_BYTES, dtype=t.uint8, device=self.device)
         self._host_results = t.zeros(slots * self.RESULT_BYTES, dtype=t.uint8, pin_memory=True)
+        self._host_results_np = self._host_results.numpy()
         dev = ctypes.c_void_p()
         _lib.call("drk_mapped_ptr", self._host_results.data_ptr(), ctypes.byref(dev))
         self._host_results_dev = int(dev.value)
@@ -170,7 +171,7 @@ class DeviceState:
     def fetch_host_results(self, slots: int) -> np.ndarray:
         """Wait for the stream, then the raw bytes of host result slots [0, slots)."""
         self.synchronize()
-        return self._host_results.numpy()[: slots * self.RESULT_BYTES].copy()
+        return self._host_results_np[: slots * self.RESULT_BYTES].copy()
 
     def fetch_results(self, slots: int) -> np.ndarray:
         """Copy result slots [0, slots) to pinned host memory and wait (raw bytes)."""
@@ -185,6 +186,10 @@ class DeviceState:
     def synchronize(self):
         if self.backend == "cuda":
             _lib.call("drk_stream_synchronize", self.index, self.handle)
+
+    def results_view(self) -> np.ndarray:
+        """The mapped host result slots (valid after synchronize())."""
+        return self._host_results_np
 
     # -- asynchronous host transfers ---------------------------------------------
     def copy_stream(self, direction: str):

@@ -251,3 +251,13 @@ def test_scan_view_catalogue(meta_rt):
     li = _lowered(meta_rt, [np.int32, np.int32])
     mixed = expr.trace(lambda t: t[0] * 2.5, li.value)  # int32 * 2.5 -> float64
     assert kernels.match_scan_view(mixed, li.leaves, 0, f32) is None
+
+
+def test_trace_cache_sees_globals_of_nested_functions():
+    g = {"np": np, "K": 2}
+    exec("def f(t):\n    return (lambda u: u * K)(t)\n", g)
+    leaf = expr.leaf(0, np.float64)
+    a = expr.trace_cached(g["f"], leaf, ("n",))
+    g["K"] = 7
+    b = expr.trace_cached(g["f"], leaf, ("n",))
+    assert any(c[0] == 2 for c in _consts(a)) and any(c[0] == 7 for c in _consts(b))

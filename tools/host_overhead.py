@@ -42,6 +42,28 @@ for name, f in ops.items():
         f()
     torch.cuda.synchronize()
     out[name] = round((time.perf_counter() - t0) / reps * 1e6, 1)
+# C1: dot at 2^24 over 2 segments (one batched launch), per API call and kernel alone
+rt2 = sr.Runtime(2, devices=[0])
+n1 = 1 << 24
+cx = sr.DistributedVector(rt2, n1, dtype=np.float32)
+cy = sr.DistributedVector(rt2, n1, dtype=np.float32)
+repro.fill_unit(cx, 1, 0)
+repro.fill_unit(cy, 1, n1)
+for _ in range(50):
+    B.dot_product(cx, cy)
+torch.cuda.synchronize()
+reps = 1000
+t0 = time.perf_counter()
+for _ in range(reps):
+    B.dot_product(cx, cy)
+out["c1_dot_2^24_p2"] = round((time.perf_counter() - t0) / reps * 1e6, 1)
+from paper_2406_00158_b200 import kernels  # noqa: E402
+with kernels.profile() as prof:
+    for _ in range(200):
+        B.dot_product(cx, cy)
+    torch.cuda.synchronize()
+ks = prof.summary()
+out["c1_kernel_us"] = {k: round(v[1] / v[0] * 1e3, 1) for k, v in ks.items()}
 print(json.dumps({"us_per_call": out, "n": n}), flush=True)
 if "--profile" in sys.argv:
     for name, f in ops.items():
