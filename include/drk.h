@@ -33,7 +33,7 @@ enum { DRK_ADD = 0, DRK_MUL = 1, DRK_MIN = 2, DRK_MAX = 3 };
 /* generator kinds for drk_generate (reference repro.py:21-40) */
 enum { DRK_GEN_UNIFORM = 0, DRK_GEN_MOD = 1 };
 /* library error codes (disjoint from cudaError_t values, which stay below 1000) */
-enum { DRK_E_ARG = 1001, DRK_E_DTYPE = 1002, DRK_E_SCRATCH = 1003, DRK_E_JIT = 1004 };
+enum { DRK_E_ARG = 1001, DRK_E_DTYPE = 1002, DRK_E_SCRATCH = 1003, DRK_E_JIT = 1004, DRK_E_COMM = 1005 };
 
 int drk_version(void);
 const char* drk_last_error(void);
@@ -190,6 +190,39 @@ int drk_reduce_batch(int dtype, int op, int nseg, const void* const* xs, const i
 /* bench.py:87-90 dot_product over every segment pair a GPU holds, one launch */
 int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
                   void* results, void* scratch, int device, void* stream);
+
+/* ---- cross-GPU combine of a reduce (reference algorithms.py:146-149) ---------------------
+ * The driver's ascending fold of per-segment partials, on the device.  partials[k] is the
+ * device address (own memory, NVLink peer memory, or an all-gathered buffer) of segment k's
+ * partial in the accumulator type (drk_acc_dtype); each is rounded to numpy's reduce dtype
+ * P = drk_partial_dtype(dtype, op) (float32 stays float32, int32 sums widen to int64) and
+ * folded from init (a P value) in segment order:  r = ((init op P0) op P1) ...
+ * The result (a P value) goes to result_dev and/or result_host_mapped (mapped pinned host
+ * memory).  count <= DRK_FOLD_MAX. */
+#define DRK_FOLD_MAX 64
+int drk_partial_dtype(int dtype, int op);
+int drk_reduce_fold(int dtype, int op, const void* const* partials, int count, const void* init,
+                    void* result_dev, void* result_host_mapped, int device, void* stream);
+
+/* A single-process NCCL communicator over ndev (<= DRK_COMM_MAX_DEV) distinct GPUs
+ * (ncclCommInitAll; NCCL is loaded at run time, drk_comm_available() says whether it can be).
+ * drk_comm_allgather: GPU i contributes `words` 8-byte words from send[i] and receives
+ * ndev * words into recv[i], on streams[i] (one NCCL group).
+ * drk_comm_reduce: the whole combine of one reduce in one call — all-gather of every GPU's
+ * `words` partial slots (slots[i], padded), then on every GPU the drk_reduce_fold of the
+ * gathered partials in segment order (order[k] = gathered word of segment k): every GPU ends
+ * with the same result (result_dev[i], array nullable), independent of NCCL's reduction
+ * order; GPU 0 also stores it into result_host_mapped (nullable). */
+#define DRK_COMM_MAX_DEV 16
+int drk_comm_available(void);
+int drk_comm_version(void);
+int drk_comm_create(int ndev, const int* devices, void** comm);
+int drk_comm_destroy(void* comm);
+int drk_comm_allgather(void* comm, const void* const* send, void* const* recv, size_t words,
+                       void* const* streams);
+int drk_comm_reduce(void* comm, int dtype, int op, const void* const* slots, void* const* gather, size_t words,
+                    const int* order, int count, const void* init, void* const* result_dev,
+                    void* result_host_mapped, void* const* streams);
 
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
  * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),

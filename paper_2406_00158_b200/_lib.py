@@ -21,7 +21,7 @@ CSRC_DIR = os.path.join(_HERE, "csrc")
 F32, F64, I32, I64 = 0, 1, 2, 3
 ADD, MUL, MIN, MAX = 0, 1, 2, 3
 GEN_UNIFORM, GEN_MOD = 0, 1
-E_ARG, E_DTYPE, E_SCRATCH, E_JIT = 1001, 1002, 1003, 1004
+E_ARG, E_DTYPE, E_SCRATCH, E_JIT, E_COMM = 1001, 1002, 1003, 1004, 1005
 
 DTYPE_CODE = {
     np.dtype(np.float32): F32,
@@ -93,6 +93,15 @@ SIGNATURES = {
                                  _int, _int, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "drk_carry_fold": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _vp, _vp, _vp, _int,
                               _vp]),
+    "drk_partial_dtype": (_int, [_int, _int]),
+    "drk_reduce_fold": (_int, [_int, _int, ctypes.POINTER(_vp), _int, _vp, _vp, _vp, _int, _vp]),
+    "drk_comm_available": (_int, []),
+    "drk_comm_version": (_int, []),
+    "drk_comm_create": (_int, [_int, ctypes.POINTER(_int), ctypes.POINTER(_vp)]),
+    "drk_comm_destroy": (_int, [_vp]),
+    "drk_comm_allgather": (_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, ctypes.POINTER(_vp)]),
+    "drk_comm_reduce": (_int, [_vp, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, ctypes.POINTER(_int),
+                               _int, _vp, ctypes.POINTER(_vp), _vp, ctypes.POINTER(_vp)]),
     "drk_sort_keys": (_int, [_int, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
     "drk_sort_pairs": (_int, [_int, _vp, _vp, _vp, _vp, _i64, _vp, ctypes.POINTER(_sz), _int, _vp]),
     "drk_gather": (_int, [_int, _vp, _vp, _vp, _i64, _int, _vp]),
@@ -190,6 +199,8 @@ CARRY_MAX = 64  # drk.h DRK_CARRY_MAX: predecessors one drk_carry_fold call fold
 SCAN_CHAINED = 1  # drk.h DRK_SCAN_CHAINED
 SCAN_SEGS = 16  # drk.h DRK_SCAN_SEGS
 RED_SEGS = 16  # drk.h DRK_RED_SEGS
+FOLD_MAX = 64  # drk.h DRK_FOLD_MAX: partials one drk_reduce_fold folds
+COMM_MAX_DEV = 16  # drk.h DRK_COMM_MAX_DEV
 VIEW_PRODUCT, VIEW_AFFINE = 1, 2  # drk.h DRK_VIEW_*
 JIT_WORDS = 16  # drk_device.cuh DRK_JIT_WORDS: 8-byte words of a fused scan loader
 

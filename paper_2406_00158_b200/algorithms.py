@@ -233,6 +233,10 @@ def reduce(r, init=0, op=add):
         if not pieces:
             return init.item() if isinstance(init, np.generic) else init
         plan = plans.store(key, dvs, _ReducePlan(_require_runtime(runtime_of(r), "reduce"), pieces, op))
+    if plan.rt.reduce_combine != "host":
+        r = plan.fold_on_device(init)
+        if r is not None:
+            return r
     partials = plan.run()
     acc = init
     for p in partials:
@@ -307,6 +311,97 @@ class _ReducePlan:
         return out
 
 
+    def _device_init(self, init):
+        """init as a scalar of the partial dtype P when the host fold `op.fn(init, p)` stays
+        in P (numpy promotion of a Python or same-dtype scalar), else None (host fold)."""
+        if self.opcode is None or not self.lowered:
+            return None
+        vdts = {lw.value.dtype for lw in self.lowered}
+        if len(vdts) != 1:
+            return None
+        P = _partial_dtype(self.op, vdts.pop())
+        if P not in _lib.DTYPE_CODE:
+            return None
+        try:
+            with np.errstate(all="ignore"):
+                probe = self.op.fn(init, P.type(0))
+                iv = P.type(init)
+        except (OverflowError, TypeError, ValueError):
+            return None
+        if np.asarray(probe).dtype != P:
+            return None
+        return P, iv
+
+    def fold_on_device(self, init):
+        """The reduce folded on the device (rt.reduce_combine "device" or "nccl"): every
+        segment's partial is reduced into a device slot of its GPU, then
+          device: the first GPU waits for the others (CUDA events) and folds the partials
+                  from their memory over NVLink (drk_reduce_fold);
+          nccl:   one drk_comm_reduce — an NCCL all-gather of every GPU's partial slots, then
+                  every GPU folds them in segment order (the result on every GPU);
+        and one mapped-memory read of the result.  The fold is the reference driver's
+        ascending fold in numpy's reduce dtype (algorithms.py:146-149), so the value is the
+        host fold's bit for bit.  None when the host must fold (see _device_init)."""
+        from .runtime import torch
+
+        di = self._device_init(init)
+        if di is None or len(self.lowered) > _lib.FOLD_MAX:
+            return None
+        P, iv = di
+        rt = self.rt
+        mode = rt.reduce_combine
+        for st, k in self.need:
+            st.ensure_results(k)
+        states = sorted(rt.device_states, key=lambda s: s.index)
+        pos = {id(s): i for i, s in enumerate(states)}
+        cnt = {}
+        place = []  # (state, slot) of each segment, in segment order
+        for lw in self.lowered:
+            st = rt.state_of(lw.rank if lw.rank is not None else 0)
+            j = cnt.get(id(st), 0)
+            cnt[id(st)] = j + 1
+            place.append((st, j))
+        words = max(cnt.values())
+        ndev = len(states)
+        for st in states:
+            st.combine_slots(8 * words * (ndev + 1))
+        if self.batch is not None:
+            self.batch.launch(result_ptr=self.batch.st.combine_slots(0).data_ptr())
+        else:
+            launches = {}
+            for lw, (st, j) in zip(self.lowered, place):
+                launch = launches.setdefault(id(st), Launch(st))
+                node = lw.value
+                run_reduce(node, lw.leaves, lw.length, self.opcode, None, launch, j,
+                           result_ptr=st.combine_slots(0).data_ptr() + 8 * j)
+        code = _lib.DTYPE_CODE[self.lowered[0].value.dtype]
+        initbuf = _lib.scalar_buffer(iv, P)
+        st0 = states[0]
+        host = st0.host_result_dev_ptr(0)
+        if mode == "nccl":
+            comm = rt.comm()
+            vp = ctypes.c_void_p
+            send = (vp * ndev)(*[s.combine_slots(0).data_ptr() for s in states])
+            recv = (vp * ndev)(*[s.combine_slots(0).data_ptr() + 8 * words for s in states])
+            streams = (vp * ndev)(*[s.handle for s in states])
+            order = (ctypes.c_int * len(place))(*[pos[id(s)] * words + j for s, j in place])
+            _lib.call("drk_comm_reduce", comm, code, self.opcode, send, recv, words, order, len(place),
+                      ctypes.addressof(initbuf), None, host, streams)
+        else:
+            t = torch()
+            for s in states[1:]:
+                if s is not st0 and id(s) in cnt:
+                    ev = t.cuda.Event()
+                    ev.record(s.stream)
+                    st0.stream.wait_event(ev)
+            parts = (ctypes.c_void_p * len(place))(*[s.combine_slots(0).data_ptr() + 8 * j for s, j in place])
+            _lib.call("drk_reduce_fold", code, self.opcode, parts, len(place), ctypes.addressof(initbuf), None, host,
+                      st0.index, st0.handle)
+        raw = st0.fetch_host_results(1)
+        r = np.frombuffer(raw[: P.itemsize].tobytes(), dtype=P)[0]
+        return r.item()
+
+
 def _segment_partials(rt, pieces, op):
     return _ReducePlan(rt, pieces, op).run()
 
@@ -318,19 +413,22 @@ class _BatchReduce:
 
     __slots__ = ("st", "kind", "code", "opcode", "m", "xs", "ys", "ns", "handles", "dtypes", "total")
 
-    def launch(self):
+    def launch(self, result_ptr=None):
+        """Enqueue the batched kernel; results into the mapped host slots [0, m) of the
+        GPU, or into device memory at result_ptr (8-byte slots)."""
         from .runtime import await_pending
 
         st = self.st
         await_pending(st, self.handles)
         launch = Launch(st)
         scratch = st.reduce_batch_scratch(self.m)
+        res = st.host_result_dev_ptr(0) if result_ptr is None else result_ptr
         if self.kind == "reduce":
             kernels.launch_kernel("drk_reduce_batch", launch, self.total, self.code, self.opcode, self.m, self.xs,
-                                  self.ns, st.host_result_dev_ptr(0), scratch.data_ptr())
+                                  self.ns, res, scratch.data_ptr())
         else:
             kernels.launch_kernel("drk_dot_batch", launch, self.total, self.code, self.m, self.xs, self.ys, self.ns,
-                                  st.host_result_dev_ptr(0), scratch.data_ptr())
+                                  res, scratch.data_ptr())
         order = [(st, j, dt) for j, dt in enumerate(self.dtypes)]
         return order, {id(st): launch}, {id(st): self.m}
 

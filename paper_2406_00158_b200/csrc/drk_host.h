@@ -40,21 +40,24 @@ extern int g_scan_l2_subs;  // sub-tiles per L2 tile (0: 8 = 160 KB for 4-byte t
 extern int g_scan_l2_pre;   // sub-tiles scanned prefix-free during the look-back
 extern int g_scan_l2_ring;  // TMA ring slots of the L2 re-scan (2 or 3)
 extern int g_scan_debug;    // ScanParams::debug (experiments only)
-extern int g_scan_stagger;  // ns between first-wave tile starts of the L2 scan (-1: automatic)
+extern int g_scan_stagger;
+extern int g_scan_smem_pad;    // extra dynamic smem of the L2 scan (caps CTAs per SM): experiments
+extern int g_scan_rescan_pol;  // ScanParams::rescan_pol  // ns between first-wave tile starts of the L2 scan (-1: automatic)
 extern thread_local int g_chain_launch;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
 extern void* g_scan_trace;  // debug: per-tile timestamps of the next scans
 
 int sm_count(int device);
 
 template <class K> static int occupancy(K kernel, int block, size_t smem) {
-  static std::unordered_map<const void*, int> cache;
+  static std::unordered_map<uint64_t, int> cache;
   std::lock_guard<std::mutex> lk(g_mu);
-  auto it = cache.find((const void*)kernel);
+  const uint64_t key = ((uint64_t)(uintptr_t)kernel << 20) ^ (uint64_t)smem ^ ((uint64_t)block << 40);
+  auto it = cache.find(key);
   if (it != cache.end()) return it->second;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, block, smem) != cudaSuccess || n < 1)
     n = 1;
-  cache[(const void*)kernel] = n;
+  cache[key] = n;
   return n;
 }
 

@@ -140,6 +140,8 @@ int g_scan_l2_pre = 2;
 int g_scan_l2_ring = 3;
 int g_scan_debug = 0;
 int g_scan_stagger = -1;
+int g_scan_smem_pad = 0;
+int g_scan_rescan_pol = 0;
 thread_local int g_chain_launch = 0;
 void* g_scan_trace = nullptr;
 
@@ -204,6 +206,18 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_l2_min")) {
     old = g_scan_l2_min;
     g_scan_l2_min = value;
+  } else if (!strcmp(name, "scan_smem_pad")) {
+    old = g_scan_smem_pad;
+    g_scan_smem_pad = value;
+  } else if (!strcmp(name, "scan_rescan_pol")) {
+    old = g_scan_rescan_pol;
+    g_scan_rescan_pol = value;
+  } else if (!strcmp(name, "l2_persist_mb")) {
+    // persisting-L2 set-aside of the current device (evict_last lines): experiments
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    old = (int)(cur >> 20);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)value << 20);
   } else if (!strcmp(name, "scan_sub")) {
     old = g_scan_sub;
     if (value >= 1 && value <= 4) g_scan_sub = value;

@@ -18,6 +18,8 @@ static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int 
   const int64_t nt = (p.n + tile - 1) / tile;
   if (nt > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
   p.ntiles = (u32)nt;
+  smem += g_scan_smem_pad;
+  p.rescan_pol = g_scan_rescan_pol;
   DRK_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   // With more than two waves of tiles, every CTA lets a chained successor launch as soon as
   // it starts (a no-op unless the next kernel is a DRK_SCAN_CHAINED scan): all of this grid

@@ -72,6 +72,14 @@ class AggregateTaskError(RuntimeError):
         super().__init__(f"{len(self.failures)} task(s) failed (indices {idx}): {msgs}")
 
 
+# how reduce combines per-segment partials across GPUs (algorithms.py:146-149, the driver's
+# ascending fold): "host" — every GPU stores its partials into mapped pinned memory and the
+# host folds them; "device" — the first GPU folds them from peer memory (NVLink) and stores
+# one result; "nccl" — an NCCL all-gather of the partials, then every GPU folds them in
+# segment order (all-reduce semantics, the result on every GPU).  Same value every way.
+REDUCE_COMBINES = ("host", "device", "nccl")
+
+
 def default_locale_count() -> int:
     """SEGRANGE_LOCALES if set, else the number of visible GPUs (at least 1), capped at 16."""
     env = os.environ.get(LOCALES_ENV)
@@ -156,6 +164,18 @@ class DeviceState:
         _lib.call("drk_mapped_ptr", self._host_results.data_ptr(), ctypes.byref(dev))
         self._host_results_dev = int(dev.value)
         self._result_slots = slots
+
+    def combine_slots(self, nbytes: int):
+        """Device buffer of the cross-GPU reduce combine (partials and the all-gathered
+        partials, algorithms._ReducePlan.fold_on_device), kept apart from the scan's result
+        slots."""
+        buf = getattr(self, "_combine", None)
+        if buf is None or buf.numel() < nbytes:
+            t = torch()
+            with t.cuda.stream(self.stream):
+                buf = t.zeros(max(nbytes, 4096), dtype=t.uint8, device=self.device)
+            self._combine = buf
+        return buf
 
     def result_ptr(self, slot: int) -> int:
         return self._results.data_ptr() + slot * self.RESULT_BYTES
@@ -355,7 +375,7 @@ class Runtime:
     each task.  ``devices`` picks the CUDA devices (default: all visible)."""
 
     def __init__(self, locale_count: int | None = None, worker_mode: str = "threads", devices=None,
-                 backend: str = "cuda"):
+                 backend: str = "cuda", reduce_combine: str | None = None):
         if locale_count is None:
             locale_count = default_locale_count()
         if locale_count < 1:
@@ -364,6 +384,12 @@ class Runtime:
             raise ValueError(f"unknown worker mode {worker_mode!r}")
         if backend not in ("cuda", "meta"):
             raise ValueError(f"unknown backend {backend!r}")
+        if reduce_combine is None:
+            reduce_combine = os.environ.get("DRK_REDUCE_COMBINE", "host")
+        if reduce_combine not in REDUCE_COMBINES:
+            raise ValueError(f"unknown reduce_combine {reduce_combine!r} (one of {', '.join(REDUCE_COMBINES)})")
+        self.reduce_combine = reduce_combine
+        self._comm = None
         self.locale_count = int(locale_count)
         self.worker_mode = worker_mode
         self.backend = backend
@@ -546,6 +572,18 @@ class Runtime:
         raise TypeError(f"cannot copy {type(obj).__name__}; expected ndarray, tensor or StorageHandle")
 
     # -- lifecycle -----------------------------------------------------------------
+    def comm(self):
+        """The runtime's single-process NCCL communicator over its GPUs (ncclCommInitAll,
+        created on first use; drk_comm_create), for reduce_combine="nccl"."""
+        self._check_open()
+        if self._comm is None:
+            devs = sorted(self._states)
+            arr = (ctypes.c_int * len(devs))(*devs)
+            h = ctypes.c_void_p()
+            _lib.call("drk_comm_create", len(devs), arr, ctypes.byref(h))
+            self._comm = h.value
+        return self._comm
+
     def close(self):
         with self._lock:
             if self._closed:
@@ -557,6 +595,12 @@ class Runtime:
                     st.synchronize()
                 except Exception:  # pragma: no cover - teardown
                     pass
+            if self._comm is not None:
+                try:
+                    _lib.call("drk_comm_destroy", self._comm)
+                except Exception:  # pragma: no cover - teardown
+                    pass
+                self._comm = None
 
     def __enter__(self):
         return self

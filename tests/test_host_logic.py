@@ -213,3 +213,16 @@ class TestViewsAlgebra:
         ta = [len(s) for s in views.trim_segments(a.segments(), 0, n)]
         tb = [len(s) for s in views.trim_segments(b.segments(), 0, n)]
         assert boundaries(lens) == boundaries(ta) | boundaries(tb)
+
+
+def test_reduce_combine_option():
+    """Runtime(reduce_combine=...) accepts the three combine modes and rejects others."""
+    import paper_2406_00158_b200 as sr
+    from paper_2406_00158_b200.runtime import REDUCE_COMBINES
+
+    assert REDUCE_COMBINES == ("host", "device", "nccl")
+    for mode in REDUCE_COMBINES:
+        assert sr.Runtime(2, backend="meta", reduce_combine=mode).reduce_combine == mode
+    assert sr.Runtime(2, backend="meta").reduce_combine in REDUCE_COMBINES
+    with pytest.raises(ValueError):
+        sr.Runtime(2, backend="meta", reduce_combine="allreduce")
