@@ -45,12 +45,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES = {"dot": 8, "triad": 12, "scan": 8, "copy": 8, "scale": 8, "add": 12, "black_scholes": 24,
+         "black_scholes_fast": 24,
          "scan_affine": 8, "scan_product": 12, "reduce": 4}
 # the libdrk entry points each pipeline launches (kernels.profile keys; batched variants run
 # when a GPU holds several segments)
 KERNEL_OF = {"dot": ("drk_dot", "drk_dot_batch"), "triad": ("drk_triad",), "scan": ("drk_scan", "drk_scan_batch"),
              "copy": ("drk_copy",), "scale": ("drk_scale",), "add": ("drk_add",),
-             "black_scholes": ("drk_black_scholes",), "scan_affine": ("drk_scan_view:affine",),
+             "black_scholes": ("drk_black_scholes",), "black_scholes_fast": ("drk_black_scholes:fast",),
+             "scan_affine": ("drk_scan_view:affine",),
              "scan_product": ("drk_scan_view:product",), "reduce": ("drk_reduce", "drk_reduce_batch")}
 STEP_WORKLOADS = ("dot", "triad", "scan")
 
@@ -66,7 +68,8 @@ def parse(argv=None):
     p.add_argument("--share-gpu", action="store_true",
                    help="shp test mode: every GPU's segments on GPU 0 (also DRK_BENCH_SHARE_GPU=1)")
     p.add_argument("--workloads", default=",".join(STEP_WORKLOADS),
-                   help="comma list from dot,triad,scan,copy,scale,add,black_scholes,scan_affine,scan_product,"
+                   help="comma list from dot,triad,scan,copy,scale,add,black_scholes (fp64-internal pricing, the "
+                        "reference's precision),black_scholes_fast (fp32 SFU tier),scan_affine,scan_product,"
                         "reduce")
     p.add_argument("--e2e-log2n", type=int, default=None, help="elements per GPU for e2e (default: same)")
     p.add_argument("--no-e2e", action="store_true")
@@ -245,7 +248,7 @@ def cpu_measure(log2n, workloads, threads, min_seconds, steps=None, warmup=0):
     b = O.unit_doubles(1, 0, n).astype(np.float32)
     c = O.unit_doubles(1, n, n).astype(np.float32)
     cols = None
-    if "black_scholes" in workloads:
+    if "black_scholes" in workloads or "black_scholes_fast" in workloads:
         from paper_2406_00158_b200.bench import BS_RANGES
 
         cols = [O.uniform_doubles(1, k * n, n, lo, hi).astype(np.float32) for k, (lo, hi) in enumerate(BS_RANGES.values())]
@@ -263,7 +266,7 @@ def cpu_measure(log2n, workloads, threads, min_seconds, steps=None, warmup=0):
                 O.triad(b, c, 0.0, p, threads)
             elif w in ("scale", "add"):
                 O.triad(b, c, 3.0, p, threads)
-            elif w == "black_scholes":
+            elif w in ("black_scholes", "black_scholes_fast"):  # the reference prices in fp64
                 O.black_scholes_prices(cols, np.float32, p, threads)
             elif w == "scan_affine":  # the reference materialises the view, then scans it
                 O.scan((np.float32(2.5) * c + np.float32(1.0)).astype(np.float32), p, np.float32, threads=threads)
@@ -410,7 +413,7 @@ def main(argv=None):
     repro.fill_unit(b, 1, off)          # global vector b = unit_doubles(1, 0, N)
     repro.fill_unit(c, 1, N + off)      # global vector c = unit_doubles(1, N, N)
     bs_cols = None
-    if "black_scholes" in workloads:
+    if "black_scholes" in workloads or "black_scholes_fast" in workloads:
         bs_cols = []
         for k, (lo, hi) in enumerate(B.BS_RANGES.values()):
             v = sr.DistributedVector(rt, vlen, dtype=dt)
@@ -436,8 +439,10 @@ def main(argv=None):
             B.stream_scale(a, c)
         elif w == "add":
             B.stream_add(a, b, c)
-        elif w == "black_scholes":
+        elif w == "black_scholes":  # fp64 internals, the reference's precision (bench.py:109)
             B.black_scholes_prices(a, *bs_cols)
+        elif w == "black_scholes_fast":  # fp32 SFU tier (rel <= 1e-5 of the reference)
+            B.black_scholes_prices(a, *bs_cols, precision="fast")
         elif w == "scan_affine":  # inclusive_scan(transform(c, 2.5 c + 1)): fused, 8 B/elem
             A.inclusive_scan(views.transform(c, lambda x: 2.5 * x + 1.0), a)
         elif w == "scan_product":  # inclusive_scan(transform(zip(b, c), t0 * t1)): fused, 12 B/elem

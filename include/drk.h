@@ -76,10 +76,20 @@ int drk_add(int dtype, void* out, const void* a, const void* b, int64_t n, int d
 /* out[i] = b[i] + alpha * c[i]        — bench.stream_triad, bench.py:93-99 (two roundings) */
 int drk_triad(int dtype, void* out, const void* b, const void* c, int64_t n, const void* alpha,
               int device, void* stream);
-/* out[i] = European call price         — bench.black_scholes_call/prices, bench.py:106-126 */
+/* out[i] = European call price         — bench.black_scholes_call/prices, bench.py:106-126.
+ * The reference's arithmetic operation by operation: for fp32 columns only spot is widened
+ * (bench.py:109), so vol, exp(-rT), the drift and strike*discount are fp32 operations (numpy's
+ * float32 exp replayed bit for bit) and the log, the normal CDFs and the price fp64, rounded
+ * once to dtype.  drk_black_scholes_ex with DRK_BS_FAST is the fast tier: fp32 columns priced
+ * in fp32 with SFU approximations (rel <= 1e-5 of the reference; HBM-bound at 2^28 options),
+ * fp64 columns in fp64 with fma contraction. */
+enum { DRK_BS_FAST = 1 };
 int drk_black_scholes(int dtype, void* out, const void* spot, const void* strike,
                       const void* rate, const void* volatility, const void* expiry, int64_t n,
                       int device, void* stream);
+int drk_black_scholes_ex(int dtype, int flags, void* out, const void* spot, const void* strike,
+                         const void* rate, const void* volatility, const void* expiry, int64_t n,
+                         int device, void* stream);
 /* Device twin of repro.py:21-40 (splitmix64 window [start, start+n) of `seed`):
  *   DRK_GEN_UNIFORM: out[i] = dtype(a + (b - a) * unit_double)   (a=0,b=1: unit_doubles)
  *   DRK_GEN_MOD:     out[i] = dtype(int64(bits % (uint64)a) + (int64)b)

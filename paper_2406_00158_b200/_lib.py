@@ -71,6 +71,7 @@ SIGNATURES = {
     "drk_add": (_int, [_int, _vp, _vp, _vp, _i64, _int, _vp]),
     "drk_triad": (_int, [_int, _vp, _vp, _vp, _i64, _vp, _int, _vp]),
     "drk_black_scholes": (_int, [_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp]),
+    "drk_black_scholes_ex": (_int, [_int, _int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _int, _vp]),
     "drk_generate": (_int, [_int, _vp, _i64, _u64, _u64, _int, _dbl, _dbl, _int, _vp]),
     "drk_reduce_scratch_bytes": (_sz, []),
     "drk_acc_dtype": (_int, [_int, _int]),
@@ -202,6 +203,7 @@ RED_SEGS = 16  # drk.h DRK_RED_SEGS
 FOLD_MAX = 64  # drk.h DRK_FOLD_MAX: partials one drk_reduce_fold folds
 COMM_MAX_DEV = 16  # drk.h DRK_COMM_MAX_DEV
 VIEW_PRODUCT, VIEW_AFFINE = 1, 2  # drk.h DRK_VIEW_*
+BS_FAST = 1  # drk.h DRK_BS_FAST
 JIT_WORDS = 16  # drk_device.cuh DRK_JIT_WORDS: 8-byte words of a fused scan loader
 
 # sort / gather / bounds also take unsigned keys (drk.h DRK_U32 / DRK_U64)

@@ -128,8 +128,16 @@ def _bs_host(spot, strike, rate, volatility, expiry):
 
 black_scholes_call = expr.DeviceFunction("black_scholes", 5, _bs_result_dtype, _bs_host)
 black_scholes_call.__doc__ = """European call price C = S*Phi(d1) - K*exp(-rT)*Phi(d2); vol = sigma*sqrt(T) <= 0
-gives the discounted intrinsic value (reference bench.py:106-116).  Inside a traced
-element function it becomes the fused drk_black_scholes kernel."""
+gives the discounted intrinsic value (reference bench.py:106-116).  Priced in fp64 and rounded
+once to the result dtype, like the reference prices fp32 columns in float64 (bench.py:109).
+Inside a traced element function it becomes the fused drk_black_scholes kernel."""
+
+black_scholes_call_fast = expr.DeviceFunction("black_scholes_fast", 5, _bs_result_dtype, _bs_host)
+black_scholes_call_fast.__doc__ = """black_scholes_call with fp32 columns priced in fp32 (SFU
+exp2/log2/rcp, one erfc fit for Phi: rel <= 1e-5 against the fp64 formula): the fast tier,
+HBM-bound on B200 (drk_black_scholes_ex DRK_BS_FAST).  fp64 columns are priced in fp64."""
+
+BS_PRECISIONS = ("reference", "fast")
 
 
 def norm_cdf(x):
@@ -138,13 +146,17 @@ def norm_cdf(x):
     return 0.5 * (1.0 + erf(x / np.sqrt(2.0)))
 
 
-def black_scholes_prices(out, spot, strike, rate, volatility, expiry):
-    """out[i] = call price of option i, element-wise over the zipped inputs."""
-    algorithms.for_each(
-        views.zip(out, spot, strike, rate, volatility, expiry),
-        lambda t: (black_scholes_call(t[1], t[2], t[3], t[4], t[5]), None, None, None, None, None),
-        vectorized=True,
-    )
+def black_scholes_prices(out, spot, strike, rate, volatility, expiry, precision="reference"):
+    """out[i] = call price of option i, element-wise over the zipped inputs (reference
+    bench.py:119-126).  precision "reference" prices in fp64 like the reference; "fast"
+    prices fp32 columns in fp32 (black_scholes_call_fast)."""
+    if precision not in BS_PRECISIONS:
+        raise ValueError(f"precision must be one of {BS_PRECISIONS}, got {precision!r}")
+    if precision == "fast":
+        fn = lambda t: (black_scholes_call_fast(t[1], t[2], t[3], t[4], t[5]), None, None, None, None, None)  # noqa: E731
+    else:
+        fn = lambda t: (black_scholes_call(t[1], t[2], t[3], t[4], t[5]), None, None, None, None, None)  # noqa: E731
+    algorithms.for_each(views.zip(out, spot, strike, rate, volatility, expiry), fn, vectorized=True)
 
 
 # ----------------------------------------------------------------------------------------

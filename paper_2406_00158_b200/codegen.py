@@ -280,7 +280,9 @@ class Emitter:
             return self.tmp(T, f"drk::m_{op}({args[0]})")
         if op == "where":
             return self.tmp(T, f"({args[0]} ? {args[1]} : {args[2]})")
-        if op == "call:black_scholes":
+        if op == "call:black_scholes":  # the reference's fp64-internal pricing (drk::BSRef)
+            return self.tmp(T, f"drk::BSRef<{T}>::price({', '.join(args)})")
+        if op == "call:black_scholes_fast":
             return self.tmp(T, f"drk::BSMath<{T}>::price({', '.join(args)})")
         raise JitError(f"no device code for operation {op}")
 

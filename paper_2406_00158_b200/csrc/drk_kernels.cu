@@ -142,6 +142,8 @@ int g_scan_debug = 0;
 int g_scan_stagger = -1;
 int g_scan_smem_pad = 0;
 int g_scan_rescan_pol = 0;
+int g_scan_exp = 0;
+int g_scan_keep_tail = 1;
 thread_local int g_chain_launch = 0;
 void* g_scan_trace = nullptr;
 
@@ -209,6 +211,12 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_smem_pad")) {
     old = g_scan_smem_pad;
     g_scan_smem_pad = value;
+  } else if (!strcmp(name, "scan_keep_tail")) {
+    old = g_scan_keep_tail;
+    g_scan_keep_tail = value;
+  } else if (!strcmp(name, "scan_exp")) {
+    old = g_scan_exp;
+    g_scan_exp = value;
   } else if (!strcmp(name, "scan_rescan_pol")) {
     old = g_scan_rescan_pol;
     g_scan_rescan_pol = value;
@@ -354,7 +362,7 @@ template <class T> struct TriadF {
   }
 };
 
-template <class T> struct BlackScholesF {
+template <class T, class M = BSMath<T>> struct BlackScholesF {
   struct Params {
     T* out;
     const T *S, *K, *r, *v, *t;
@@ -374,11 +382,11 @@ template <class T> struct BlackScholesF {
   static __device__ __forceinline__ void store(const Params& p, i64 i, const Regs& g) {
     T o[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) o[e] = BSMath<T>::price(g.S[e], g.K[e], g.r[e], g.v[e], g.t[e]);
+    for (int e = 0; e < E; ++e) o[e] = M::price(g.S[e], g.K[e], g.r[e], g.v[e], g.t[e]);
     stv<T, E>(p.out + i, o);
   }
   static __device__ __forceinline__ void scalar(const Params& p, i64 i) {
-    p.out[i] = BSMath<T>::price(p.S[i], p.K[i], p.r[i], p.v[i], p.t[i]);
+    p.out[i] = M::price(p.S[i], p.K[i], p.r[i], p.v[i], p.t[i]);
   }
 };
 
@@ -518,19 +526,30 @@ extern "C" int drk_triad(int dtype, void* out, const void* b, const void* c, int
   });
 }
 
-extern "C" int drk_black_scholes(int dtype, void* out, const void* S, const void* K, const void* r,
-                                 const void* v, const void* t, int64_t n, int device, void* stream) {
+extern "C" int drk_black_scholes_ex(int dtype, int flags, void* out, const void* S, const void* K, const void* r,
+                                    const void* v, const void* t, int64_t n, int device, void* stream) {
   if (n > 0 && (need(out, "drk_black_scholes", "out") || need(S, "drk_black_scholes", "spot") ||
                 need(K, "drk_black_scholes", "strike") || need(r, "drk_black_scholes", "rate") ||
                 need(v, "drk_black_scholes", "volatility") || need(t, "drk_black_scholes", "expiry")))
     return DRK_E_ARG;
+  if (flags & ~DRK_BS_FAST) return set_error(DRK_E_ARG, "drk_black_scholes: unknown flags");
   DRK_DISPATCH_FLOAT(dtype, "drk_black_scholes", T, {
-    typename BlackScholesF<T>::Params p{(T*)out, (const T*)S, (const T*)K, (const T*)r, (const T*)v,
-                                        (const T*)t};
     const bool al = aligned16(out) && aligned16(S) && aligned16(K) && aligned16(r) && aligned16(v) &&
                     aligned16(t);
-    return launch_map<BlackScholesF<T>>(p, n, al, device, stream, "drk_black_scholes");
+    if (flags & DRK_BS_FAST) {
+      typename BlackScholesF<T>::Params p{(T*)out, (const T*)S, (const T*)K, (const T*)r, (const T*)v,
+                                          (const T*)t};
+      return launch_map<BlackScholesF<T>>(p, n, al, device, stream, "drk_black_scholes");
+    }
+    typename BlackScholesF<T, BSRef<T>>::Params p{(T*)out, (const T*)S, (const T*)K, (const T*)r, (const T*)v,
+                                                   (const T*)t};
+    return launch_map<BlackScholesF<T, BSRef<T>>>(p, n, al, device, stream, "drk_black_scholes");
   });
+}
+
+extern "C" int drk_black_scholes(int dtype, void* out, const void* S, const void* K, const void* r,
+                                 const void* v, const void* t, int64_t n, int device, void* stream) {
+  return drk_black_scholes_ex(dtype, 0, out, S, K, r, v, t, n, device, stream);
 }
 
 extern "C" int drk_generate(int dtype, void* out, int64_t n, uint64_t seed, uint64_t start, int kind,

@@ -63,6 +63,8 @@ def launch_kernel(name, launch_ctx, n, *args, key=None):
     e.record(launch_ctx.state.stream)
     if key is None:
         key = name[:-3] if name.endswith("_ex") else name  # drk_scan_ex is reported as drk_scan
+        if name == "drk_black_scholes_ex" and args[1] & _lib.BS_FAST:
+            key = "drk_black_scholes:fast"
     _PROFILE.setdefault(key, []).append((s, e, n))
 
 
@@ -183,10 +185,11 @@ def match_map(node, leaves, out_dtype):
                     kb, kc, alpha = x.value, p.value, q.value
                     return ("drk_triad", lambda out, n, ptrs, L: (
                         code, out, ptrs[kb], ptrs[kc], n, _keep(L, _scalar_arg(alpha, T))))
-    if node.op == "call:black_scholes" and T.kind == "f" and all(_is_leaf(a, leaves) and a.dtype == T
-                                                                 for a in node.args):
+    if node.op in ("call:black_scholes", "call:black_scholes_fast") and T.kind == "f" and all(
+            _is_leaf(a, leaves) and a.dtype == T for a in node.args):
         ks = [a.value for a in node.args]
-        return ("drk_black_scholes", lambda out, n, ptrs, L: (code, out, *[ptrs[k] for k in ks], n))
+        flags = _lib.BS_FAST if node.op == "call:black_scholes_fast" else 0
+        return ("drk_black_scholes_ex", lambda out, n, ptrs, L: (code, flags, out, *[ptrs[k] for k in ks], n))
     return None
 
 

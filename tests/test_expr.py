@@ -7,7 +7,7 @@ from hypothesis import given, settings
 from hypothesis import strategies as st
 
 import paper_2406_00158_b200 as sr
-from paper_2406_00158_b200 import codegen, expr, kernels, views
+from paper_2406_00158_b200 import _lib, codegen, expr, kernels, views
 from paper_2406_00158_b200 import bench as B
 
 DTYPES = [np.float32, np.float64, np.int32, np.int64]
@@ -111,7 +111,11 @@ def test_catalogue_matching(meta_rt, fn, kernel):
 def test_black_scholes_catalogue(meta_rt):
     lw = _lowered(meta_rt, [np.float32] * 6)
     res = expr.trace(lambda t: (B.black_scholes_call(t[1], t[2], t[3], t[4], t[5]),) + (None,) * 5, lw.value)
-    assert kernels.match_map(res[0], lw.leaves, np.float32)[0] == "drk_black_scholes"
+    name, args = kernels.match_map(res[0], lw.leaves, np.float32)
+    assert name == "drk_black_scholes_ex" and args(0, 1, [0] * 6, None)[1] == 0  # fp64 internal
+    res = expr.trace(lambda t: (B.black_scholes_call_fast(t[1], t[2], t[3], t[4], t[5]),) + (None,) * 5, lw.value)
+    name, args = kernels.match_map(res[0], lw.leaves, np.float32)
+    assert name == "drk_black_scholes_ex" and args(0, 1, [0] * 6, None)[1] == _lib.BS_FAST
 
 
 def test_codegen_compiles_map_reduce_scan(meta_rt):

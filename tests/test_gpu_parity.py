@@ -145,7 +145,13 @@ def test_black_scholes(case, rt_pool, gold):
     B.black_scholes_prices(out, *[_vec(rt, c) for c in cols])
     got = out.to_numpy()
     ref = gold.arrays[case["id"]]
-    np.testing.assert_allclose(got, ref, rtol=REL[case["dtype"]], atol=0)
+    if dt == np.float32:
+        # the reference's arithmetic replayed (fp32 vol/discount/drift, numpy's float32 exp,
+        # fp64 CDFs): bit-exact (the fast fp32 tier is checked at rel 1e-5 in test_api_gpu and
+        # test_config_parity_gpu)
+        assert np.array_equal(got, ref)
+    else:
+        np.testing.assert_allclose(got, ref, rtol=REL[case["dtype"]], atol=0)
 
 
 @_sel("copy")
