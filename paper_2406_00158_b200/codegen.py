@@ -63,8 +63,24 @@ _lock = threading.Lock()
 _modules: dict = {}
 
 
+_HEADER_DIGEST = None
+
+
+def _header_digest() -> bytes:
+    """Hash of the device header the generated sources include: a cubin cached on disk is
+    reused only when both the source and drk_device.cuh are unchanged."""
+    global _HEADER_DIGEST
+    if _HEADER_DIGEST is None:
+        h = hashlib.sha256()
+        for fn in ("drk_device.cuh",):
+            with open(os.path.join(_lib.CSRC_DIR, fn), "rb") as fh:
+                h.update(fh.read())
+        _HEADER_DIGEST = h.digest()
+    return _HEADER_DIGEST
+
+
 def compile_module(source: str, name: str) -> Module:
-    digest = hashlib.sha256(source.encode()).hexdigest()[:32]
+    digest = hashlib.sha256(_header_digest() + source.encode()).hexdigest()[:32]
     with _lock:
         mod = _modules.get(digest)
         if mod is not None:

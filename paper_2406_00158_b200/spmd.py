@@ -180,13 +180,33 @@ def reduce(local, init, op, group: Group):
         vdt = np.asarray(parts[0]).dtype
         for p in parts:
             partial = p if partial is None else op.fn(partial, p)
-    code_dt = vdt if vdt is not None else np.dtype(getattr(local, "dtype", np.float64))
+    code_dt = vdt if vdt is not None else _value_dtype(local)
     L = A._partial_dtype(op, code_dt) if code_dt in _lib.DTYPE_CODE else code_dt
     acc = init
     for q in gather_pairs(partial, L, group, _state_of(rt, local)):
         if q is not None:
             acc = op.fn(acc, q)
     return acc.item() if isinstance(acc, np.generic) else acc
+
+
+def _value_dtype(local):
+    """Element dtype of a rank-local range that may hold no elements: the vector's dtype, or
+    for a view the dtype of its lowered (empty) segment expression — so an empty rank decodes
+    and folds the gathered partials in the same dtype as the ranks that have elements."""
+    dt = getattr(local, "dtype", None)
+    if dt is not None:
+        return np.dtype(dt)
+    from . import algorithms as A
+    from .views import lower
+
+    for seg in A.segments_of(local):
+        try:
+            value = lower(seg).value
+        except Exception:  # pragma: no cover - a view that cannot lower has no device dtype
+            continue
+        if not isinstance(value, tuple):
+            return np.dtype(value.dtype)
+    return np.dtype(np.float64)
 
 
 def _state_of(rt, local):

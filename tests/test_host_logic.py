@@ -226,3 +226,20 @@ def test_reduce_combine_option():
     assert sr.Runtime(2, backend="meta").reduce_combine in REDUCE_COMBINES
     with pytest.raises(ValueError):
         sr.Runtime(2, backend="meta", reduce_combine="allreduce")
+
+
+def test_spmd_value_dtype_of_empty_view():
+    """An empty rank-local view still reports its element dtype (spmd.reduce decodes the
+    gathered partials in it, like the ranks that hold elements)."""
+    import paper_2406_00158_b200 as sr
+    from paper_2406_00158_b200 import spmd, views
+
+    rt = sr.Runtime(2, backend="meta")
+    v = sr.DistributedVector(rt, 0, dtype=np.float32)
+    w = sr.DistributedVector(rt, 0, dtype=np.float32)
+    assert spmd._value_dtype(v) == np.float32
+    assert spmd._value_dtype(w) == np.float32
+    # a view with (trailing empty) segments lowers to its element dtype
+    x = sr.DistributedVector(rt, 1, dtype=np.float32)
+    assert spmd._value_dtype(views.transform(views.zip(x, x), lambda t: t[0] * t[1])) == np.float32
+    assert spmd._value_dtype(views.transform(x, lambda e: e * 2)) == np.float32
