@@ -235,9 +235,10 @@ int drk_comm_reduce(void* comm, int dtype, int op, const void* const* slots, voi
                     void* result_host_mapped, void* const* streams);
 
 /* ---- sort (reference algorithms.py:315-432) ------------------------------------------------
- * Device radix sort (CUB) of one contiguous buffer (a segment, or a sample-sort chunk),
- * plus the splitter search of the distributed sample sort; the runtime moves the runs
- * between GPUs (peer copies) exactly as the reference's redistribution does.
+ * This library's LSD radix sort (8-bit digits; upsweep / scan / stable downsweep per pass)
+ * of one contiguous buffer (a segment, or a sample-sort chunk), n < 2^31, in numpy's order
+ * (NaN last), plus the splitter search of the distributed sample sort; the runtime moves
+ * the runs between GPUs (peer copies) exactly as the reference's redistribution does.
  * With scratch == NULL, *scratch_bytes receives the required scratch size. */
 int drk_sort_keys(int dtype, void* keys, void* alt, int64_t n, void* scratch, size_t* scratch_bytes,
                   int device, void* stream);

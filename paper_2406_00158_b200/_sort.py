@@ -2,13 +2,13 @@
 
 The reference's phases, each mapped to device work on the segments' own GPUs:
 
-  1. local sort of every segment           CUB radix sort in place (drk_sort_keys /
+  1. local sort of every segment           LSD radix sort in place (drk_sort_keys /
                                             drk_sort_pairs for a key function), per GPU stream
   2. P-1 evenly spaced samples per segment drk_gather of the sample positions, D2H (tiny)
   3. splitters from the pooled samples     host (P·(P-1) values, like the reference's driver)
   4. counts per (segment, chunk)           drk_sort_bounds: P-1 binary searches per sorted run
   5. redistribution into per-locale chunks peer copies over NVLink, pulled by the chunk's GPU
-  6. sort of every chunk                    CUB radix sort (stable: runs arrive in segment order)
+  6. sort of every chunk                    LSD radix sort (stable: runs arrive in segment order)
   7. chunks swept back over the segments    peer copies, pulled by the segment's GPU
 
 Ordering between GPUs is by CUDA events (a stream waits for the phase before it on every
