@@ -176,6 +176,14 @@ def check(rc: int, func: str) -> None:
 _FUNCS = {}
 
 
+def fn(name: str):
+    """The bound entry point `name` (cached): hot paths call it directly and check rc."""
+    f = _FUNCS.get(name)
+    if f is None:
+        f = _FUNCS[name] = getattr(load(), name)
+    return f
+
+
 def call(name: str, *args) -> None:
     """Call an int-returning entry point and raise DrkError on failure."""
     fn = _FUNCS.get(name)

@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import operator
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -158,14 +159,29 @@ def for_each(r, fn, vectorized: bool = False) -> None:
             _collect_writes(result, lw.target, writes)
             if writes:
                 work.append((rt.state_of(writes[0][0].handle.locale), writes, lw.leaves, lw.length))
-        plan = plans.store(key, dvs, (rt, work))
-    rt, work = plan
+        plan = plans.store(key, dvs, [rt, work, None])
+    _run_map_plan(plan, key is not None)
+
+
+def _run_map_plan(plan, cached=True):
+    """Run a cached map plan [rt, work, bound]: after the first run every launch whose
+    arguments are fixed is re-issued as one direct call (kernels.BoundMap)."""
+    rt, work, bound = plan
+    if bound and kernels._PROFILE is None:
+        for b in bound:
+            b()
+        if _SYNC_ALGORITHMS:
+            rt.synchronize()
+        return
     launches = []
     for st, writes, leaves, length in work:
         launch = Launch(st)
         run_map(writes, leaves, length, launch)
         launches.append(launch)
     _finish(rt, launches)
+    if bound is None and cached:
+        bs = [kernels.bind_map(writes, leaves, length, st) for st, writes, leaves, length in work]
+        plan[2] = bs if all(b is not None for b in bs) else ()  # () = launch through run_map
 
 
 def _collect_writes(result, target, writes):
@@ -286,7 +302,7 @@ class _ReducePlan:
         for st, k in self.need:
             st.ensure_results(k)  # before any launch: growing the slot buffer reallocates it
         if self.batch is not None:
-            order, launches, slots = self.batch.launch()
+            return self.batch.run()
         else:
             order, launches, slots = [], {}, {}
             for lw in self.lowered:
@@ -411,18 +427,41 @@ class _BatchReduce:
     product of two for dot): one drk_reduce_batch / drk_dot_batch launch, its argument arrays
     built once."""
 
-    __slots__ = ("st", "kind", "code", "opcode", "m", "xs", "ys", "ns", "handles", "dtypes", "total")
+    __slots__ = ("st", "kind", "code", "opcode", "m", "xs", "ys", "ns", "handles", "dtypes", "total", "decode",
+                 "fmt", "op")
+
+    def run(self):
+        """Launch, wait, and the partials in numpy's reduce dtype (the C1 hot path: argument
+        arrays, the result layout and the decoding are fixed at plan time)."""
+        self.launch()
+        st = self.st
+        st.synchronize()
+        vals = struct.unpack_from(self.fmt, st._host_results_np)
+        return [cast(v) for cast, v in zip(self.decode, vals)]
 
     def launch(self, result_ptr=None):
         """Enqueue the batched kernel; results into the mapped host slots [0, m) of the
         GPU, or into device memory at result_ptr (8-byte slots)."""
-        from .runtime import await_pending
-
         st = self.st
-        await_pending(st, self.handles)
-        launch = Launch(st)
+        for h in self.handles:
+            if h._pending:
+                from .runtime import await_pending
+
+                await_pending(st, self.handles)
+                break
         scratch = st.reduce_batch_scratch(self.m)
         res = st.host_result_dev_ptr(0) if result_ptr is None else result_ptr
+        if kernels._PROFILE is None:  # the common case: one direct call
+            if self.kind == "reduce":
+                rc = _lib.fn("drk_reduce_batch")(self.code, self.opcode, self.m, self.xs, self.ns, res,
+                                                 scratch.data_ptr(), st.index, st.handle)
+            else:
+                rc = _lib.fn("drk_dot_batch")(self.code, self.m, self.xs, self.ys, self.ns, res, scratch.data_ptr(),
+                                              st.index, st.handle)
+            if rc:
+                _lib.check(rc, "drk_reduce_batch" if self.kind == "reduce" else "drk_dot_batch")
+            return None
+        launch = Launch(st)
         if self.kind == "reduce":
             kernels.launch_kernel("drk_reduce_batch", launch, self.total, self.code, self.opcode, self.m, self.xs,
                                   self.ns, res, scratch.data_ptr())
@@ -434,10 +473,10 @@ class _BatchReduce:
 
 
 def _batch_reduce_plan(rt, lowered, opcode):
-    """A _BatchReduce for the pieces, or None when they do not qualify (one piece, several
-    GPUs, or an expression outside the catalogue)."""
+    """A _BatchReduce for the pieces, or None when they do not qualify (more than
+    DRK_RED_SEGS pieces, several GPUs, or an expression outside the catalogue)."""
     m = len(lowered)
-    if not 1 < m <= _lib.RED_SEGS:
+    if not 1 <= m <= _lib.RED_SEGS:  # one segment too: the lean fixed-argument launch
         return None
     states = {id(rt.state_of(lw.rank if lw.rank is not None else 0)) for lw in lowered}
     if len(states) != 1:
@@ -457,7 +496,29 @@ def _batch_reduce_plan(rt, lowered, opcode):
     b.ys = (ctypes.c_void_p * m)(*[p[3] for p in plans_]) if b.kind == "dot" else None
     b.handles = [lf.handle for lw in lowered for lf in lw.leaves if lf.handle is not None]
     b.dtypes = [lw.value.dtype for lw in lowered]
+    # result slot j holds the accumulator (drk_acc_dtype) of segment j; the reference's partial
+    # is that value in numpy's reduce dtype (float32 sums are accumulated in fp64, then rounded)
+    fmt, decode = "<", []
+    for dt in b.dtypes:
+        A = _lib.acc_dtype(dt, opcode)
+        fmt += {"f8": "d", "f4": "f4x", "i8": "q", "i4": "i4x"}[A.kind + str(A.itemsize)]
+        decode.append(_PARTIAL_OF[(opcode, np.dtype(dt))])
+    b.fmt, b.decode = fmt, decode
     return b
+
+
+def _partial_caster(opcode, dt):
+    ufunc = {_lib.ADD: np.add, _lib.MUL: np.multiply, _lib.MIN: np.minimum, _lib.MAX: np.maximum}[opcode]
+    return _partial_dtype(BinaryOp(ufunc, None, ufunc), dt).type
+
+
+class _PartialOf(dict):
+    def __missing__(self, key):
+        v = self[key] = _partial_caster(*key)
+        return v
+
+
+_PARTIAL_OF = _PartialOf()
 
 
 # ----------------------------------------------------------------------------------------
@@ -1039,10 +1100,16 @@ def copy(src, dst) -> None:
             if isinstance(tgt, ReadOnly):
                 raise TypeError(f"cannot write through read-only {tgt.what}")
             work.append((ls, tgt, rt.state_of(d.rank)))
-        plan = (rt, work)
+        plan = [rt, work, None]
         if key is not None:
             plans.CACHE.put(key, dvs, plan)
-    rt, work = plan
+    rt, work, bound = plan
+    if bound and kernels._PROFILE is None:
+        for b in bound:
+            b()
+        if _SYNC_ALGORITHMS:
+            rt.synchronize()
+        return
     launches = []
     for ls, d, st in work:
         if st is None:
@@ -1052,6 +1119,10 @@ def copy(src, dst) -> None:
         run_map([(d, ls.value)], ls.leaves, ls.length, launch)
         launches.append(launch)
     _finish(rt, launches)
+    if bound is None and key is not None:
+        bs = [kernels.bind_map([(d, ls.value)], ls.leaves, ls.length, st) if st is not None else None
+              for ls, d, st in work]
+        plan[2] = bs if bs and all(b is not None for b in bs) else ()
 
 
 def _copy_to_host(rt, ls, piece, launches):

@@ -431,6 +431,15 @@ def _leaf_sig(leaves, used):
 
 
 def run_map(writes, leaves, ptrs, n, launch):
+    mod, kernel, grid, buf, nbytes = map_launch(writes, leaves, ptrs, n, launch.device)
+    from .kernels import launch_jit
+
+    launch_jit(mod, kernel, grid, BLOCK, 0, buf, nbytes, launch, n)
+
+
+def map_launch(writes, leaves, ptrs, n, device):
+    """(module, kernel, grid, packed argument buffer, its size) of the generated map kernel
+    for these writes (compiled and cached on first use)."""
     key = (tuple((np.dtype(t.dtype).str, node.key()) for t, node in writes),
            _leaf_sig(leaves, expr.leaves_used(tuple(n_ for _, n_ in writes))))
     plan = _MAP_PLANS.get(key)
@@ -455,10 +464,8 @@ def run_map(writes, leaves, ptrs, n, launch):
         grid = (n // E + BLOCK * U - 1) // (BLOCK * U) + 1
     else:
         kernel = "drk_map_striped"
-        grid = _grid(mod, kernel, (n + BLOCK * 4 - 1) // (BLOCK * 4), launch.device)
-    from .kernels import launch_jit
-
-    launch_jit(mod, kernel, int(min(grid, 0x7FFFFFFF)), BLOCK, 0, buf, len(blob), launch, n)
+        grid = _grid(mod, kernel, (n + BLOCK * 4 - 1) // (BLOCK * 4), device)
+    return mod, kernel, int(min(grid, 0x7FFFFFFF)), buf, len(blob)
 
 
 # ----------------------------------------------------------------------------------------

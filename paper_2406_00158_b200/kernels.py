@@ -221,6 +221,63 @@ def run_map(writes, leaves, n, launch: Launch):
     _release_peers(leaves, launch)
 
 
+class BoundMap:
+    """One map launch with every argument fixed (a plan's lowered segment on its own GPU):
+    re-issued as a single entry-point call.  Used by cached for_each / copy plans; profiled
+    runs and launches that need per-call work (host slices, peer reads, aliasing
+    snapshots) take run_map instead."""
+
+    __slots__ = ("fn", "args", "name", "handles", "keep", "state")
+
+    def __call__(self):
+        for h in self.handles:
+            if h._pending:
+                from .runtime import await_pending
+
+                await_pending(self.state, self.handles)
+                break
+        rc = self.fn(*self.args)
+        if rc:
+            _lib.check(rc, self.name)
+
+
+def bind_map(writes, leaves, n, state):
+    """A BoundMap for run_map(writes, leaves, n) on `state`'s GPU, or None when the launch
+    needs per-call work."""
+    if n == 0 or not writes:
+        return None
+    for lf in leaves:
+        if lf.kind == "host" or (lf.kind == "array" and lf.device != state.index):
+            return None
+    for tgt, _ in writes:
+        if tgt.handle is None:
+            return None
+        for lf in leaves:
+            if lf.kind == "array" and lf.handle is tgt.handle and lf.start != tgt.start:
+                return None  # an aliasing snapshot per call
+    launch = Launch(state)
+    ptrs = [lf.ptr() if lf.kind == "array" else 0 for lf in leaves]
+    b = BoundMap()
+    b.state = state
+    b.handles = [t.handle for t, _ in writes] + [lf.handle for lf in leaves if lf.kind == "array" and lf.handle is not None]
+    m = match_map(writes[0][1], leaves, writes[0][0].dtype) if len(writes) == 1 else None
+    if m is not None:
+        name, build = m
+        b.name = name
+        b.fn = _lib.fn(name)
+        b.args = (*build(writes[0][0].ptr(), n, ptrs, launch), state.index, state.handle)
+    else:
+        from . import codegen
+
+        mod, kernel, grid, buf, nbytes = codegen.map_launch(writes, leaves, ptrs, n, state.index)
+        b.name = "drk_jit_launch"
+        b.fn = _lib.fn("drk_jit_launch")
+        b.args = (mod.handle, kernel.encode(), grid, codegen.BLOCK, 0, buf, nbytes, state.index, state.handle)
+        launch.keep.append(buf)
+    b.keep = launch.keep
+    return b
+
+
 def _release_peers(leaves, launch: Launch):
     """After a kernel that reads other GPUs' memory over NVLink: their streams wait for it, so
     nothing they run later (a write, or the reuse of freed memory) overtakes the read."""
