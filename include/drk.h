@@ -200,6 +200,16 @@ int drk_reduce_batch(int dtype, int op, int nseg, const void* const* xs, const i
 /* bench.py:87-90 dot_product over every segment pair a GPU holds, one launch */
 int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
                   void* results, void* scratch, int device, void* stream);
+/* The batched reductions with completion words: once segment k's result is final (and
+ * visible to the host), flags[k] (nullable; nseg 8-byte words, typically mapped pinned host
+ * memory beside `results`) is set to `epoch`.  drk_wait_flags spins on the host until every
+ * word equals epoch — lower latency than a stream synchronisation for a scalar result; the
+ * stream is still checked for errors while waiting. */
+int drk_reduce_batch_ex(int dtype, int op, int nseg, const void* const* xs, const int64_t* ns, void* results,
+                        void* flags, uint64_t epoch, void* scratch, int device, void* stream);
+int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                     void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream);
+int drk_wait_flags(const void* host_flags, int count, uint64_t epoch, int device, void* stream);
 
 /* ---- cross-GPU combine of a reduce (reference algorithms.py:146-149) ---------------------
  * The driver's ascending fold of per-segment partials, on the device.  partials[k] is the

@@ -80,6 +80,11 @@ SIGNATURES = {
     "drk_scan_scratch_bytes": (_sz, [_int, _int, _i64]),
     "drk_scan": (_int, [_int, _int, _int, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _int, _vp]),
     "drk_reduce_batch": (_int, [_int, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp, _int, _vp]),
+    "drk_reduce_batch_ex": (_int, [_int, _int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp, _u64, _vp,
+                                   _int, _vp]),
+    "drk_dot_batch_ex": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp,
+                                _u64, _vp, _int, _vp]),
+    "drk_wait_flags": (_int, [_vp, _int, _u64, _int, _vp]),
     "drk_dot_batch": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp,
                              _int, _vp]),
     "drk_scan_batch_scratch_bytes": (_sz, [_int, _int, _int, ctypes.POINTER(_i64)]),

@@ -432,10 +432,34 @@ class _BatchReduce:
 
     def run(self):
         """Launch, wait, and the partials in numpy's reduce dtype (the C1 hot path: argument
-        arrays, the result layout and the decoding are fixed at plan time)."""
-        self.launch()
+        arrays, the result layout and the decoding are fixed at plan time).  The kernel marks
+        each result final with a completion word in mapped memory, and the host waits on
+        those words (drk_wait_flags) rather than synchronising the whole stream."""
         st = self.st
-        st.synchronize()
+        if kernels._PROFILE is not None:
+            self.launch()
+            st.synchronize()
+        else:
+            for h in self.handles:
+                if h._pending:
+                    from .runtime import await_pending
+
+                    await_pending(st, self.handles)
+                    break
+            fh, fd, epoch = st.completion_flags()
+            scratch = st.reduce_batch_scratch(self.m).data_ptr()
+            res = st.host_result_dev_ptr(0)
+            if self.kind == "reduce":
+                rc = _lib.fn("drk_reduce_batch_ex")(self.code, self.opcode, self.m, self.xs, self.ns, res, fd, epoch,
+                                                    scratch, st.index, st.handle)
+            else:
+                rc = _lib.fn("drk_dot_batch_ex")(self.code, self.m, self.xs, self.ys, self.ns, res, fd, epoch,
+                                                 scratch, st.index, st.handle)
+            if rc:
+                _lib.check(rc, "drk_reduce_batch" if self.kind == "reduce" else "drk_dot_batch")
+            rc = _lib.fn("drk_wait_flags")(fh, self.m, epoch, st.index, st.handle)
+            if rc:
+                _lib.check(rc, "drk_wait_flags")
         vals = struct.unpack_from(self.fmt, st._host_results_np)
         return [cast(v) for cast, v in zip(self.decode, vals)]
 

@@ -664,7 +664,8 @@ extern "C" int drk_reduce(int dtype, int op, const void* x, int64_t n, void* res
 // 8-byte slot per segment, `scratch` nseg x drk_reduce_scratch_bytes().
 template <class LD, class Op>
 static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const int64_t* ns, const bool* vec_ok,
-                               void* results, void* scratch, int device, void* stream, const char* what) {
+                               void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream,
+                               const char* what) {
   typedef typename WideAcc<typename LD::V, Op>::type A;
   if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, std::string(what) + ": nseg out of range");
   if (!results || !scratch) return set_error(DRK_E_ARG, std::string(what) + ": null results/scratch");
@@ -695,15 +696,17 @@ static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const in
     b.vec_ok[k] = vec_ok[k] ? 1 : 0;
     b.s[k] = carve_reduce((char*)scratch + (size_t)k * sbytes);
     b.result[k] = (A*)((char*)results + 8 * (size_t)k);
+    b.flag[k] = flags ? (u64*)flags + k : nullptr;
   }
+  b.epoch = epoch;
   b.cta_first[nseg] = first;
   kern<<<first, BLOCK, 0, (cudaStream_t)stream>>>(b);
   return epilogue(what);
 }
 
 template <class T>
-static int reduce_batch_op(int op, int nseg, const void* const* xs, const int64_t* ns, void* results, void* scratch,
-                           int device, void* stream) {
+static int reduce_batch_op(int op, int nseg, const void* const* xs, const int64_t* ns, void* results, void* flags,
+                           uint64_t epoch, void* scratch, int device, void* stream) {
   typename IdentLoad<T>::Params ps[DRK_RED_SEGS];
   bool v[DRK_RED_SEGS];
   if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_reduce_batch: nseg out of range");
@@ -714,23 +717,29 @@ static int reduce_batch_op(int op, int nseg, const void* const* xs, const int64_
   }
   const char* w = "drk_reduce_batch";
   switch (op) {
-    case DRK_ADD: return launch_reduce_batch<IdentLoad<T>, OpAdd>(nseg, ps, ns, v, results, scratch, device, stream, w);
-    case DRK_MUL: return launch_reduce_batch<IdentLoad<T>, OpMul>(nseg, ps, ns, v, results, scratch, device, stream, w);
-    case DRK_MIN: return launch_reduce_batch<IdentLoad<T>, OpMin>(nseg, ps, ns, v, results, scratch, device, stream, w);
-    case DRK_MAX: return launch_reduce_batch<IdentLoad<T>, OpMax>(nseg, ps, ns, v, results, scratch, device, stream, w);
+    case DRK_ADD: return launch_reduce_batch<IdentLoad<T>, OpAdd>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
+    case DRK_MUL: return launch_reduce_batch<IdentLoad<T>, OpMul>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
+    case DRK_MIN: return launch_reduce_batch<IdentLoad<T>, OpMin>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
+    case DRK_MAX: return launch_reduce_batch<IdentLoad<T>, OpMax>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
   }
   return set_error(DRK_E_ARG, "drk_reduce_batch: unknown op");
 }
 
-extern "C" int drk_reduce_batch(int dtype, int op, int nseg, const void* const* xs, const int64_t* ns, void* results,
-                                void* scratch, int device, void* stream) {
+extern "C" int drk_reduce_batch_ex(int dtype, int op, int nseg, const void* const* xs, const int64_t* ns,
+                                   void* results, void* flags, uint64_t epoch, void* scratch, int device,
+                                   void* stream) {
   if (!xs || !ns) return set_error(DRK_E_ARG, "drk_reduce_batch: null segment arrays");
   DRK_DISPATCH(dtype, "drk_reduce_batch", T,
-               { return reduce_batch_op<T>(op, nseg, xs, ns, results, scratch, device, stream); });
+               { return reduce_batch_op<T>(op, nseg, xs, ns, results, flags, epoch, scratch, device, stream); });
 }
 
-extern "C" int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
-                             void* results, void* scratch, int device, void* stream) {
+extern "C" int drk_reduce_batch(int dtype, int op, int nseg, const void* const* xs, const int64_t* ns, void* results,
+                                void* scratch, int device, void* stream) {
+  return drk_reduce_batch_ex(dtype, op, nseg, xs, ns, results, nullptr, 0, scratch, device, stream);
+}
+
+extern "C" int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                                void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream) {
   if (!xs || !ys || !ns) return set_error(DRK_E_ARG, "drk_dot_batch: null segment arrays");
   if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_dot_batch: nseg out of range");
   DRK_DISPATCH(dtype, "drk_dot_batch", T, {
@@ -741,9 +750,39 @@ extern "C" int drk_dot_batch(int dtype, int nseg, const void* const* xs, const v
       ps[k] = typename ProdLoad<T>::Params{(const T*)xs[k], (const T*)ys[k]};
       v[k] = aligned16(xs[k]) && aligned16(ys[k]);
     }
-    return launch_reduce_batch<ProdLoad<T>, OpAdd>(nseg, ps, ns, v, results, scratch, device, stream,
+    return launch_reduce_batch<ProdLoad<T>, OpAdd>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream,
                                                   "drk_dot_batch");
   });
+}
+
+extern "C" int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                             void* results, void* scratch, int device, void* stream) {
+  return drk_dot_batch_ex(dtype, nseg, xs, ys, ns, results, nullptr, 0, scratch, device, stream);
+}
+
+// Host-side wait for completion words written by a kernel into mapped pinned memory: spin
+// (a pause per poll) until every one of `count` words equals `epoch`; the stream is queried
+// every few thousand polls so a failed launch surfaces as its error instead of a hang.
+extern "C" int drk_wait_flags(const void* host_flags, int count, uint64_t epoch, int device, void* stream) {
+  if (count <= 0) return 0;
+  if (!host_flags) return set_error(DRK_E_ARG, "drk_wait_flags: null flags");
+  const volatile uint64_t* f = (const volatile uint64_t*)host_flags;
+  for (uint64_t spins = 1;; ++spins) {
+    int k = 0;
+    while (k < count && f[k] == epoch) ++k;
+    if (k == count) return 0;
+    __builtin_ia32_pause();
+    if ((spins & 4095) == 0) {
+      const cudaError_t e = cudaStreamQuery((cudaStream_t)stream);
+      if (e == cudaSuccess) {
+        k = 0;
+        while (k < count && f[k] == epoch) ++k;
+        if (k == count) return 0;
+        return set_error(DRK_E_ARG, "drk_wait_flags: the stream is idle but the completion words were not written");
+      }
+      if (e != cudaErrorNotReady) return cuda_status(e, "drk_wait_flags");
+    }
+  }
 }
 
 extern "C" int drk_dot(int dtype, const void* x, const void* y, int64_t n, void* result_dev, void* scratch,

@@ -177,6 +177,20 @@ class DeviceState:
             self._combine = buf
         return buf
 
+    def completion_flags(self):
+        """(host address, device address) of DRK_RED_SEGS 8-byte completion words in mapped
+        pinned memory, and the next epoch to wait for (drk_reduce_batch_ex / drk_wait_flags)."""
+        f = getattr(self, "_flags", None)
+        if f is None:
+            t = torch()
+            f = self._flags = t.zeros(_lib.RED_SEGS, dtype=t.int64, pin_memory=True)
+            dev = ctypes.c_void_p()
+            _lib.call("drk_mapped_ptr", f.data_ptr(), ctypes.byref(dev))
+            self._flags_host, self._flags_dev = f.data_ptr(), int(dev.value)
+            self._epoch = 0
+        self._epoch += 1
+        return self._flags_host, self._flags_dev, self._epoch
+
     def result_ptr(self, slot: int) -> int:
         return self._results.data_ptr() + slot * self.RESULT_BYTES
 
