@@ -55,6 +55,25 @@ def main():
         "bidir_GBps_total": round(2 * nbytes / t_both / 1e9, 2),
         "bidir_ms": round(t_both * 1e3, 2),
     }))
+    # the e2e step's pattern: two buffers each way, as whole copies and in chunks
+    h_in2 = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    h_out2 = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    d_in2 = torch.empty(n, dtype=torch.float32, device="cuda")
+    d_out2 = torch.ones(n, dtype=torch.float32, device="cuda")
+    for chunk in (0, 1 << 28, 1 << 26, 1 << 24):
+        def two_each():
+            pairs_in = [(d_in, h_in), (d_in2, h_in2)]
+            pairs_out = [(h_out, d_out), (h_out2, d_out2)]
+            step = n if chunk == 0 else chunk // 4
+            for (di, hi), (ho, do) in zip(pairs_in, pairs_out):
+                for o in range(0, n, step):
+                    with torch.cuda.stream(s1):
+                        di[o:o + step].copy_(hi[o:o + step], non_blocking=True)
+                    with torch.cuda.stream(s2):
+                        ho[o:o + step].copy_(do[o:o + step], non_blocking=True)
+        t = timed(two_each)
+        print(json.dumps({"pattern": "2x4GB each way", "chunk_bytes": chunk or nbytes,
+                          "bidir_GBps_total": round(4 * nbytes / t / 1e9, 2), "ms": round(t * 1e3, 2)}), flush=True)
 
 
 if __name__ == "__main__":
