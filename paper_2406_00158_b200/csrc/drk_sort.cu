@@ -152,8 +152,21 @@ __global__ void __launch_bounds__(RX_BLOCK) radix_upsweep(const K* __restrict__ 
   counts[(size_t)tid * ntiles + blockIdx.x] = c;
 }
 
+// lanes of the warp holding the same 8-bit digit (d < 256; d = 256 marks an empty slot):
+// eight ballots on the digit's bits (cheaper than MATCH.ANY on this pipe)
+__device__ __forceinline__ u32 digit_peers(int d) {
+  u32 peers = __ballot_sync(0xffffffffu, d >> 8);
+  peers = (d >> 8) ? peers : ~peers;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const u32 m = __ballot_sync(0xffffffffu, (d >> b) & 1);
+    peers &= ((d >> b) & 1) ? m : ~m;
+  }
+  return peers;
+}
+
 template <class K, bool HAS_V>
-__global__ void __launch_bounds__(RX_BLOCK) radix_downsweep(const K* __restrict__ keys_in, K* __restrict__ keys_out,
+__global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(const K* __restrict__ keys_in, K* __restrict__ keys_out,
                                                              const i64* __restrict__ vals_in, i64* __restrict__ vals_out,
                                                              i64 n, int shift, int pairs, const u32* __restrict__ offsets,
                                                              u32 ntiles) {
@@ -188,7 +201,7 @@ __global__ void __launch_bounds__(RX_BLOCK) radix_downsweep(const K* __restrict_
 #pragma unroll
   for (int j = 0; j < RX_IPT; ++j) {
     const int d = dig[j];
-    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const u32 peers = digit_peers(d);
     const u32 before = d < RX_DIGITS ? whist[w][d] : 0u;
     rank[j] = before + (u32)__popc(peers & lt);
     __syncwarp();
