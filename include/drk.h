@@ -210,6 +210,15 @@ int drk_reduce_batch_ex(int dtype, int op, int nseg, const void* const* xs, cons
 int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
                      void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream);
 int drk_wait_flags(const void* host_flags, int count, uint64_t epoch, int device, void* stream);
+/* The batched multi-device variant: every GPU's batched reduction (kind 0) or
+ * dot (kind 1) of one algorithm call in one entry.  Segments are listed device by device —
+ * counts[d] (1..DRK_RED_SEGS) of them on devices[d] / streams[d] — and device d writes its
+ * segments' results to results[d] (8-byte slots), its completion words to flags[d] (flags
+ * nullable), using scratch[d] (counts[d] x drk_reduce_scratch_bytes()).  Every device's
+ * arguments are validated before anything is enqueued. */
+int drk_reduce_multi(int kind, int dtype, int op, int ndev, const int* devices, void* const* streams,
+                     const int* counts, const void* const* xs, const void* const* ys, const int64_t* ns,
+                     void* const* results, void* const* flags, uint64_t epoch, void* const* scratch);
 
 /* ---- cross-GPU combine of a reduce (reference algorithms.py:146-149) ---------------------
  * The driver's ascending fold of per-segment partials, on the device.  partials[k] is the

@@ -85,6 +85,9 @@ SIGNATURES = {
     "drk_dot_batch_ex": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp,
                                 _u64, _vp, _int, _vp]),
     "drk_wait_flags": (_int, [_vp, _int, _u64, _int, _vp]),
+    "drk_reduce_multi": (_int, [_int, _int, _int, _int, ctypes.POINTER(_int), ctypes.POINTER(_vp), ctypes.POINTER(_int),
+                                ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_vp),
+                                ctypes.POINTER(_vp), _u64, ctypes.POINTER(_vp)]),
     "drk_dot_batch": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp,
                              _int, _vp]),
     "drk_scan_batch_scratch_bytes": (_sz, [_int, _int, _int, ctypes.POINTER(_i64)]),

@@ -381,7 +381,7 @@ class _ReducePlan:
         ndev = len(states)
         for st in states:
             st.combine_slots(8 * words * (ndev + 1))
-        if self.batch is not None:
+        if isinstance(self.batch, _BatchReduce):
             self.batch.launch(result_ptr=self.batch.st.combine_slots(0).data_ptr())
         else:
             launches = {}
@@ -496,19 +496,81 @@ class _BatchReduce:
         return order, {id(st): launch}, {id(st): self.m}
 
 
+class _MultiReduce:
+    """The segments of a reduce spread over several GPUs, each GPU's share a catalogue batch:
+    one drk_reduce_multi call enqueues every GPU's batched kernel (the multi-device variant of
+    the C ABI), the host waits on every GPU's completion words, and the partials come back in
+    segment order for the driver fold."""
+
+    __slots__ = ("states", "kind", "code", "opcode", "counts", "devices", "streams", "xs", "ys", "ns", "handles",
+                 "order", "fmts", "decode")
+
+    def run(self):
+        from .runtime import _EPOCHS, await_pending
+
+        for st, hs in self.handles:
+            for h in hs:
+                if h._pending:
+                    await_pending(st, hs)
+                    break
+        nd = len(self.states)
+        vp = ctypes.c_void_p
+        results = (vp * nd)(*[st.host_result_dev_ptr(0) for st in self.states])
+        ptrs = [st.flag_ptrs() for st in self.states]
+        flags = (vp * nd)(*[p[1] for p in ptrs])
+        scratch = (vp * nd)(*[st.reduce_batch_scratch(c).data_ptr() for st, c in zip(self.states, self.counts)])
+        epoch = next(_EPOCHS)
+        _lib.call("drk_reduce_multi", 0 if self.kind == "reduce" else 1, self.code, self.opcode, nd, self.devices,
+                  self.streams, (ctypes.c_int * nd)(*self.counts), self.xs, self.ys, self.ns, results, flags, epoch,
+                  scratch)
+        out = [None] * sum(self.counts)
+        for st, c, (fh, _), fmt, dec, ix in zip(self.states, self.counts, ptrs, self.fmts, self.decode, self.order):
+            _lib.call("drk_wait_flags", fh, c, epoch, st.index, st.handle)
+            for j, cast, v in zip(ix, dec, struct.unpack_from(fmt, st._host_results_np)):
+                out[j] = cast(v)
+        return out
+
+
 def _batch_reduce_plan(rt, lowered, opcode):
-    """A _BatchReduce for the pieces, or None when they do not qualify (more than
-    DRK_RED_SEGS pieces, several GPUs, or an expression outside the catalogue)."""
+    """A _BatchReduce (one GPU) or _MultiReduce (several) for the pieces, or None when they do
+    not qualify (more than DRK_RED_SEGS pieces on one GPU, or an expression outside the
+    catalogue)."""
     m = len(lowered)
-    if not 1 <= m <= _lib.RED_SEGS:  # one segment too: the lean fixed-argument launch
+    if m < 1 or opcode is None:
         return None
-    states = {id(rt.state_of(lw.rank if lw.rank is not None else 0)) for lw in lowered}
-    if len(states) != 1:
+    groups = {}
+    for j, lw in enumerate(lowered):
+        st = rt.state_of(lw.rank if lw.rank is not None else 0)
+        groups.setdefault(id(st), (st, []))[1].append(j)
+    if any(len(ix) > _lib.RED_SEGS for _, ix in groups.values()):
         return None
-    st = rt.state_of(lowered[0].rank if lowered[0].rank is not None else 0)
-    plans_ = [kernels.catalogue_reduce(lw.value, lw.leaves, opcode, st.index) for lw in lowered]
+    st_of = [rt.state_of(lw.rank if lw.rank is not None else 0) for lw in lowered]
+    plans_ = [kernels.catalogue_reduce(lw.value, lw.leaves, opcode, st.index) for lw, st in zip(lowered, st_of)]
     if any(p is None for p in plans_) or len({(p[0], p[1]) for p in plans_}) != 1:
         return None
+    if len(groups) > 1:
+        mb = _MultiReduce()
+        gs = sorted(groups.values(), key=lambda g: g[0].index)
+        mb.states = [g[0] for g in gs]
+        mb.order = [g[1] for g in gs]
+        mb.counts = [len(ix) for ix in mb.order]
+        mb.kind, mb.code, mb.opcode = plans_[0][0], plans_[0][1], opcode
+        flat = [j for ix in mb.order for j in ix]
+        nd, m_ = len(gs), len(flat)
+        mb.devices = (ctypes.c_int * nd)(*[st.index for st in mb.states])
+        mb.streams = (ctypes.c_void_p * nd)(*[st.handle for st in mb.states])
+        mb.xs = (ctypes.c_void_p * m_)(*[plans_[j][2] for j in flat])
+        mb.ys = (ctypes.c_void_p * m_)(*[plans_[j][3] for j in flat]) if mb.kind == "dot" else None
+        mb.ns = (ctypes.c_int64 * m_)(*[lowered[j].length for j in flat])
+        mb.handles = [(st, [lf.handle for j in ix for lf in lowered[j].leaves if lf.handle is not None])
+                      for st, ix in zip(mb.states, mb.order)]
+        mb.fmts, mb.decode = [], []
+        for ix in mb.order:
+            fmt, dec = _decode_of([lowered[j].value.dtype for j in ix], opcode)
+            mb.fmts.append(fmt)
+            mb.decode.append(dec)
+        return mb
+    st = st_of[0]
     b = _BatchReduce()
     b.st = st
     b.kind, b.code = plans_[0][0], plans_[0][1]
@@ -520,15 +582,20 @@ def _batch_reduce_plan(rt, lowered, opcode):
     b.ys = (ctypes.c_void_p * m)(*[p[3] for p in plans_]) if b.kind == "dot" else None
     b.handles = [lf.handle for lw in lowered for lf in lw.leaves if lf.handle is not None]
     b.dtypes = [lw.value.dtype for lw in lowered]
-    # result slot j holds the accumulator (drk_acc_dtype) of segment j; the reference's partial
-    # is that value in numpy's reduce dtype (float32 sums are accumulated in fp64, then rounded)
+    b.fmt, b.decode = _decode_of(b.dtypes, opcode)
+    return b
+
+
+def _decode_of(dtypes, opcode):
+    """struct format and casts of consecutive result slots: slot j holds the accumulator
+    (drk_acc_dtype) of segment j; the reference's partial is that value in numpy's reduce
+    dtype (float32 sums are accumulated in fp64, then rounded)."""
     fmt, decode = "<", []
-    for dt in b.dtypes:
+    for dt in dtypes:
         A = _lib.acc_dtype(dt, opcode)
         fmt += {"f8": "d", "f4": "f4x", "i8": "q", "i4": "i4x"}[A.kind + str(A.itemsize)]
         decode.append(_PARTIAL_OF[(opcode, np.dtype(dt))])
-    b.fmt, b.decode = fmt, decode
-    return b
+    return fmt, decode
 
 
 def _partial_caster(opcode, dt):

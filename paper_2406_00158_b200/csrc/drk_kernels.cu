@@ -140,6 +140,7 @@ namespace drk_host {
 std::mutex g_mu;
 int g_map_waves = 0;
 int g_reduce_waves = 1;
+int g_reduce_grid = 0;  // experiments: cap on the reduce grid (0: SMs x occupancy x waves)
 int g_scan_sub = 3;
 int g_scan_l2dyn = 1;
 int g_scan_l2_min = 1 << 22;
@@ -192,6 +193,9 @@ extern "C" int drk_tune(const char* name, int value) {
   if (!strcmp(name, "map_waves")) {
     old = g_map_waves;
     g_map_waves = value;
+  } else if (!strcmp(name, "reduce_grid")) {
+    old = g_reduce_grid;
+    g_reduce_grid = value;
   } else if (!strcmp(name, "reduce_waves")) {
     old = g_reduce_waves;
     g_reduce_waves = value;
@@ -687,7 +691,8 @@ static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const in
   }
   if (int rc = prologue(device, what)) return rc;
   auto kern = reduce_batch_kernel<LD, Op, BLOCK, RED_U>;
-  const int64_t cap = (int64_t)sm_count(device) * occupancy(kern, BLOCK, 0) * (g_reduce_waves > 0 ? g_reduce_waves : 1);
+  int64_t cap = (int64_t)sm_count(device) * occupancy(kern, BLOCK, 0) * (g_reduce_waves > 0 ? g_reduce_waves : 1);
+  if (g_reduce_grid > 0 && cap > g_reduce_grid) cap = g_reduce_grid;
   ReduceBatch<LD, A> b;
   memset(&b, 0, sizeof(b));
   b.nseg = nseg;
@@ -769,6 +774,39 @@ extern "C" int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, cons
 extern "C" int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
                              void* results, void* scratch, int device, void* stream) {
   return drk_dot_batch_ex(dtype, nseg, xs, ys, ns, results, nullptr, 0, scratch, device, stream);
+}
+
+// Every GPU's batched reduction of one algorithm call in one entry (the multi-device form of
+// drk_reduce_batch_ex / drk_dot_batch_ex): segments are listed device by device, counts[d] of
+// them for devices[d], and each device gets its own results / flags / scratch.  Arguments of
+// every device are validated before anything is enqueued.
+extern "C" int drk_reduce_multi(int kind, int dtype, int op, int ndev, const int* devices, void* const* streams,
+                                const int* counts, const void* const* xs, const void* const* ys, const int64_t* ns,
+                                void* const* results, void* const* flags, uint64_t epoch, void* const* scratch) {
+  const char* what = "drk_reduce_multi";
+  if (kind != 0 && kind != 1) return set_error(DRK_E_ARG, "drk_reduce_multi: kind must be 0 (reduce) or 1 (dot)");
+  if (ndev < 1 || !devices || !streams || !counts || !xs || !ns || !results || !scratch || (kind == 1 && !ys))
+    return set_error(DRK_E_ARG, "drk_reduce_multi: null argument");
+  int off = 0;
+  for (int d = 0; d < ndev; ++d) {
+    if (counts[d] < 1 || counts[d] > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_reduce_multi: count out of range");
+    if (!results[d] || !scratch[d]) return set_error(DRK_E_ARG, "drk_reduce_multi: null result / scratch");
+    for (int k = off; k < off + counts[d]; ++k)
+      if (!xs[k] || (kind == 1 && !ys[k]) || ns[k] < 1) return set_error(DRK_E_ARG, "drk_reduce_multi: bad segment");
+    off += counts[d];
+  }
+  (void)what;
+  off = 0;
+  for (int d = 0; d < ndev; ++d) {
+    void* f = flags ? flags[d] : nullptr;
+    const int rc = kind == 0 ? drk_reduce_batch_ex(dtype, op, counts[d], xs + off, ns + off, results[d], f, epoch,
+                                                   scratch[d], devices[d], streams[d])
+                             : drk_dot_batch_ex(dtype, counts[d], xs + off, ys + off, ns + off, results[d], f, epoch,
+                                                scratch[d], devices[d], streams[d]);
+    if (rc) return rc;
+    off += counts[d];
+  }
+  return 0;
 }
 
 // Host-side wait for completion words written by a kernel into mapped pinned memory: spin

@@ -19,6 +19,7 @@ logic can be exercised on machines without a GPU; it never computes.
 from __future__ import annotations
 
 import ctypes
+import itertools
 import os
 import threading
 import weakref
@@ -78,6 +79,8 @@ class AggregateTaskError(RuntimeError):
 # one result; "nccl" — an NCCL all-gather of the partials, then every GPU folds them in
 # segment order (all-reduce semantics, the result on every GPU).  Same value every way.
 REDUCE_COMBINES = ("host", "device", "nccl")
+
+_EPOCHS = itertools.count(1)  # completion-word epochs (DeviceState.completion_flags)
 
 
 def default_locale_count() -> int:
@@ -177,6 +180,12 @@ class DeviceState:
             self._combine = buf
         return buf
 
+    def flag_ptrs(self):
+        """(host address, device address) of this GPU's completion words (allocated once)."""
+        if getattr(self, "_flags", None) is None:
+            self.completion_flags()
+        return self._flags_host, self._flags_dev
+
     def completion_flags(self):
         """(host address, device address) of DRK_RED_SEGS 8-byte completion words in mapped
         pinned memory, and the next epoch to wait for (drk_reduce_batch_ex / drk_wait_flags)."""
@@ -187,9 +196,9 @@ class DeviceState:
             dev = ctypes.c_void_p()
             _lib.call("drk_mapped_ptr", f.data_ptr(), ctypes.byref(dev))
             self._flags_host, self._flags_dev = f.data_ptr(), int(dev.value)
-            self._epoch = 0
-        self._epoch += 1
-        return self._flags_host, self._flags_dev, self._epoch
+        # one process-wide sequence: a completion word never sees the same epoch twice, even
+        # when one launch writes the words of several GPUs with a shared epoch
+        return self._flags_host, self._flags_dev, next(_EPOCHS)
 
     def result_ptr(self, slot: int) -> int:
         return self._results.data_ptr() + slot * self.RESULT_BYTES
