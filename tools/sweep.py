@@ -1,5 +1,5 @@
 """C5 sweep (one GPU): reduce / transform / inclusive_scan on fp32 vectors of 2^20..2^32
-elements through the public API, against the CPU reference path (oracle port) up to 2^26.
+elements through the public API, against the CPU reference path (oracle port) up to 2^30.
 
 For each size: per-call wall time (host overhead included), kernel time from CUDA events,
 GB/s on algorithmic bytes (reduce 4, transform 8, scan 8 per element), and a
@@ -49,7 +49,7 @@ for lg in sizes:
     A.transform(x, y, lambda v: v * 2.0 + 1.0)
     seg = y.segments()[0]
     head = seg.to_numpy()[:4096] if n <= (1 << 24) else None
-    if lg <= 26:
+    if lg <= 30:
         xs = O.mod_ints(1, 0, n, 3, -1).astype(np.float32)
         cpu = {}
         for name, f in (("reduce", lambda: O.reduce(xs, threads, 0.0, np.add, threads)),
