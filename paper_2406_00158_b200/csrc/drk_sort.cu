@@ -67,47 +67,59 @@ constexpr int RX_IPT = 16;                       // keys per thread
 constexpr int RX_TILE = RX_BLOCK * RX_IPT;       // 4096 keys per tile
 constexpr int RX_DIGITS = 256;
 
+// Keys travel as their raw bit patterns (U): every step below is integer arithmetic on the
+// bits, so no floating-point operation can touch a key (signed zeros, denormals and NaN
+// payloads are moved exactly).  RadixOf<K>::to maps bits to an unsigned radix key in numpy's
+// order; canon gives the bits written back (NaNs with the sign cleared in keys-only sorts).
 template <class K> struct RadixOf;
 template <> struct RadixOf<unsigned int> {
   typedef unsigned int U;
-  static __device__ __forceinline__ U to(unsigned int k, bool) { return k; }
+  static __device__ __forceinline__ U to(U k, bool) { return k; }
+  static __device__ __forceinline__ U canon(U k) { return k; }
 };
 template <> struct RadixOf<unsigned long long> {
   typedef unsigned long long U;
-  static __device__ __forceinline__ U to(unsigned long long k, bool) { return k; }
+  static __device__ __forceinline__ U to(U k, bool) { return k; }
+  static __device__ __forceinline__ U canon(U k) { return k; }
 };
 template <> struct RadixOf<int> {
   typedef unsigned int U;
-  static __device__ __forceinline__ U to(int k, bool) { return (U)k ^ 0x80000000u; }
+  static __device__ __forceinline__ U to(U k, bool) { return k ^ 0x80000000u; }
+  static __device__ __forceinline__ U canon(U k) { return k; }
 };
 template <> struct RadixOf<long long> {
   typedef unsigned long long U;
-  static __device__ __forceinline__ U to(long long k, bool) { return (U)k ^ 0x8000000000000000ull; }
+  static __device__ __forceinline__ U to(U k, bool) { return k ^ 0x8000000000000000ull; }
+  static __device__ __forceinline__ U canon(U k) { return k; }
 };
 template <> struct RadixOf<float> {
   typedef unsigned int U;
-  static __device__ __forceinline__ U to(float k, bool pairs) {
-    U u = __float_as_uint(k);
-    if (k != k) u &= 0x7fffffffu;                      // every NaN after +inf
+  static __device__ __forceinline__ U to(U u, bool pairs) {
+    const U mag = u & 0x7fffffffu;
+    if (mag > 0x7f800000u) u = mag;                    // every NaN after +inf
     else if (pairs && u == 0x80000000u) u = 0u;        // -0.0 ranks with +0.0
     return u ^ ((u >> 31) ? 0xffffffffu : 0x80000000u);
+  }
+  static __device__ __forceinline__ U canon(U u) {
+    const U mag = u & 0x7fffffffu;
+    return mag > 0x7f800000u ? mag : u;
   }
 };
 template <> struct RadixOf<double> {
   typedef unsigned long long U;
-  static __device__ __forceinline__ U to(double k, bool pairs) {
-    U u = (U)__double_as_longlong(k);
-    if (k != k) u &= 0x7fffffffffffffffull;
+  static __device__ __forceinline__ U to(U u, bool pairs) {
+    const U mag = u & 0x7fffffffffffffffull;
+    if (mag > 0x7ff0000000000000ull) u = mag;
     else if (pairs && u == 0x8000000000000000ull) u = 0ull;
     return u ^ ((u >> 63) ? 0xffffffffffffffffull : 0x8000000000000000ull);
   }
+  static __device__ __forceinline__ U canon(U u) {
+    const U mag = u & 0x7fffffffffffffffull;
+    return mag > 0x7ff0000000000000ull ? mag : u;
+  }
 };
-// keys-only sorts write the canonical NaN (sign cleared) back
-template <class K> __device__ __forceinline__ K canonical(K k) { return k; }
-template <> __device__ __forceinline__ float canonical<float>(float k) { return k != k ? fabsf(k) : k; }
-template <> __device__ __forceinline__ double canonical<double>(double k) { return k != k ? fabs(k) : k; }
 
-template <class K> __device__ __forceinline__ int digit_of(K k, int shift, bool pairs) {
+template <class K> __device__ __forceinline__ int digit_of(typename RadixOf<K>::U k, int shift, bool pairs) {
   return (int)((RadixOf<K>::to(k, pairs) >> shift) & 0xffu);
 }
 
@@ -116,8 +128,10 @@ template <class K> __device__ __forceinline__ int digit_of(K k, int shift, bool 
 __device__ __forceinline__ int rx_index(int w, int j, int l) { return w * 32 * RX_IPT + j * 32 + l; }
 
 template <class K>
-__global__ void __launch_bounds__(RX_BLOCK) radix_upsweep(const K* __restrict__ keys, i64 n, int shift, int pairs,
-                                                           u32* __restrict__ counts, u32 ntiles) {
+__global__ void __launch_bounds__(RX_BLOCK) radix_upsweep(const typename RadixOf<K>::U* __restrict__ keys, i64 n,
+                                                           int shift, int pairs, u32* __restrict__ counts,
+                                                           u32 ntiles) {
+  typedef typename RadixOf<K>::U U;
   // per-warp histograms (shared-memory atomics, no warp matching: the count is all that is
   // needed here), summed per digit at the end
   __shared__ u32 hist[RX_WARPS][RX_DIGITS];
@@ -126,16 +140,16 @@ __global__ void __launch_bounds__(RX_BLOCK) radix_upsweep(const K* __restrict__ 
   for (int k = 0; k < RX_WARPS; ++k) hist[k][tid] = 0;
   __syncthreads();
   const i64 base = (i64)blockIdx.x * RX_TILE;
-  K key[RX_IPT];
+  U key[RX_IPT];
 #pragma unroll
   for (int j = 0; j < RX_IPT; ++j) {
     const i64 i = base + rx_index(w, j, lane);
-    key[j] = i < n ? keys[i] : K();
+    key[j] = i < n ? keys[i] : U(0);
   }
 #pragma unroll
   for (int j = 0; j < RX_IPT; ++j) {
     const i64 i = base + rx_index(w, j, lane);
-    const int d = i < n ? digit_of(key[j], shift, pairs != 0) : RX_DIGITS;
+    const int d = i < n ? digit_of<K>(key[j], shift, pairs != 0) : RX_DIGITS;
     const int d0 = __shfl_sync(0xffffffffu, d, 0);
     if (__all_sync(0xffffffffu, d == d0)) {
       // one digit for the whole warp (narrow key ranges, upper digits): one update, not 32
@@ -166,7 +180,8 @@ __device__ __forceinline__ u32 digit_peers(int d) {
 }
 
 template <class K, bool HAS_V>
-__global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(const K* __restrict__ keys_in, K* __restrict__ keys_out,
+__global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(
+    const typename RadixOf<K>::U* __restrict__ keys_in, typename RadixOf<K>::U* __restrict__ keys_out,
                                                              const i64* __restrict__ vals_in, i64* __restrict__ vals_out,
                                                              i64 n, int shift, int pairs, const u32* __restrict__ offsets,
                                                              u32 ntiles) {
@@ -174,8 +189,9 @@ __global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(const K* __restri
   __shared__ u32 tstart[RX_DIGITS];           // exclusive prefix of the tile's digit counts
   __shared__ u32 gstart[RX_DIGITS];           // global position of the tile's run of digit d
   __shared__ u32 wsum[RX_WARPS];
+  typedef typename RadixOf<K>::U U;
   extern __shared__ __align__(16) unsigned char rx_smem[];
-  K* skeys = (K*)rx_smem;
+  U* skeys = (U*)rx_smem;
   i64* svals = (i64*)(rx_smem + RX_TILE * sizeof(K));
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const u32 tile = blockIdx.x;
@@ -186,7 +202,7 @@ __global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(const K* __restri
   gstart[tid] = offsets[(size_t)tid * ntiles + tile];
   __syncthreads();
   const u32 lt = (1u << lane) - 1u;
-  K key[RX_IPT];
+  U key[RX_IPT];
   i64 val[RX_IPT];
   int dig[RX_IPT];
   u32 rank[RX_IPT];
@@ -194,18 +210,22 @@ __global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(const K* __restri
   for (int j = 0; j < RX_IPT; ++j) {
     const int li = rx_index(w, j, lane);
     const bool ok = li < valid;
-    key[j] = ok ? keys_in[base + li] : K();
+    key[j] = ok ? keys_in[base + li] : U(0);
     if constexpr (HAS_V) val[j] = ok ? vals_in[base + li] : 0;
-    dig[j] = ok ? digit_of(key[j], shift, pairs != 0) : RX_DIGITS;
+    dig[j] = ok ? digit_of<K>(key[j], shift, pairs != 0) : RX_DIGITS;
   }
+  // the warp's digit counters are read by every lane and bumped by each digit group's leader,
+  // item after item: volatile accesses keep the compiler from hoisting the next item's reads
+  // above this item's (other lanes') updates, and __syncwarp orders them between lanes
+  volatile u32* wh = whist[w];
 #pragma unroll
   for (int j = 0; j < RX_IPT; ++j) {
     const int d = dig[j];
     const u32 peers = digit_peers(d);
-    const u32 before = d < RX_DIGITS ? whist[w][d] : 0u;
+    const u32 before = d < RX_DIGITS ? wh[d] : 0u;
     rank[j] = before + (u32)__popc(peers & lt);
     __syncwarp();
-    if (d < RX_DIGITS && lane == __ffs(peers) - 1) whist[w][d] = before + (u32)__popc(peers);
+    if (d < RX_DIGITS && lane == __ffs(peers) - 1) wh[d] = before + (u32)__popc(peers);
     __syncwarp();
   }
   __syncthreads();
@@ -238,15 +258,15 @@ __global__ void __launch_bounds__(RX_BLOCK, 4) radix_downsweep(const K* __restri
     const int d = dig[j];
     if (d < RX_DIGITS) {
       const u32 pos = tstart[d] + whist[w][d] + rank[j];
-      skeys[pos] = pairs ? key[j] : canonical(key[j]);
+      skeys[pos] = pairs ? key[j] : RadixOf<K>::canon(key[j]);
       if constexpr (HAS_V) svals[pos] = val[j];
     }
   }
   __syncthreads();
   // contiguous digit runs to their global positions
   for (int i = tid; i < valid; i += RX_BLOCK) {
-    const K k = skeys[i];
-    const int d = digit_of(k, shift, pairs != 0);
+    const U k = skeys[i];
+    const int d = digit_of<K>(k, shift, pairs != 0);
     const u32 g = gstart[d] + (u32)i - tstart[d];
     keys_out[g] = k;
     if constexpr (HAS_V) vals_out[g] = svals[i];
@@ -284,12 +304,13 @@ int radix_sort(K* keys, K* alt, i64* vals, i64* vals_alt, int64_t n, bool pairs,
   i64* vsrc = vals;
   i64* vdst = vals_alt;
   for (int shift = 0; shift < (int)(8 * sizeof(K)); shift += 8) {
-    radix_upsweep<K><<<ntiles, RX_BLOCK, 0, s>>>(src, n, shift, pairs ? 1 : 0, counts, ntiles);
+    typedef typename RadixOf<K>::U U;
+    radix_upsweep<K><<<ntiles, RX_BLOCK, 0, s>>>((const U*)src, n, shift, pairs ? 1 : 0, counts, ntiles);
     drk_note_launch();
     if (int rc = drk_scan(DRK_I32, DRK_ADD, 1, counts, offsets, (int64_t)m, &zero, nullptr, nullptr, nullptr,
                           nullptr, sscr, sbytes, device, s))
       return rc;
-    down<<<ntiles, RX_BLOCK, smem, s>>>(src, dst, vsrc, vdst, n, shift, pairs ? 1 : 0, offsets, ntiles);
+    down<<<ntiles, RX_BLOCK, smem, s>>>((const U*)src, (U*)dst, vsrc, vdst, n, shift, pairs ? 1 : 0, offsets, ntiles);
     drk_note_launch();
     DRK_CHECK(cudaGetLastError());
     K* t = src; src = dst; dst = t;

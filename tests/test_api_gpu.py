@@ -617,6 +617,42 @@ class TestSort:
         with pytest.raises(ValueError):
             sr.sort(dvec(rt3, [2, 1]), strategy="bogus")
 
+    @pytest.mark.parametrize("dtype", [np.float32, np.float64])
+    def test_radix_float_edges(self, rt_pool, dtype):
+        # the radix sort's order is numpy's: -inf < negatives < -0.0 == +0.0 < positives < +inf
+        # < NaN (every NaN, either sign, last); zeros compare equal, so only their count matters
+        rng = np.random.default_rng(11)
+        base = np.array([np.inf, -np.inf, 0.0, -0.0, np.nan, -np.nan, 1e-38, -1e-38, 5e-324 if dtype == np.float64
+                         else 1e-45, np.finfo(dtype).max, np.finfo(dtype).min, 1.5, -1.5], dtype=dtype)
+        x = np.concatenate([rng.permutation(np.tile(base, 97)), (rng.standard_normal(50_000) * 100).astype(dtype)])
+        for strategy in ("sample", "gather"):
+            v = sr.DistributedVector.from_numpy(rt_pool(4), x)
+            sr.sort(v, strategy=strategy)
+            got, exp = v.to_numpy(), np.sort(x)
+            assert np.array_equal(got, exp, equal_nan=True)
+            assert np.count_nonzero(np.isnan(got[-2 * 97:])) == 2 * 97
+
+    @pytest.mark.parametrize("dtype", [np.int32, np.int64, np.uint32, np.uint64])
+    def test_radix_integer_extremes(self, rt_pool, dtype):
+        info = np.iinfo(dtype)
+        rng = np.random.default_rng(12)
+        x = np.concatenate([np.array([info.min, info.max, 0, 1, info.max - 1, info.min + 1], dtype=dtype),
+                            rng.integers(info.min, info.max, size=100_000, dtype=dtype, endpoint=True)])
+        v = sr.DistributedVector(rt_pool(3), len(x), dtype=dtype)
+        sr.copy(x, v)
+        sr.sort(v)
+        assert np.array_equal(v.to_numpy(), np.sort(x))
+
+    def test_radix_key_sort_signed_zero_ties(self, rt_pool):
+        # key values -0.0 and +0.0 are equal for argsort(kind="stable"): ties keep input order
+        x = np.array([0.0, -3.0, 3.0, -0.0, 2.0, -2.0, 0.0, -0.0] * 1000, dtype=np.float64)
+        v = sr.DistributedVector.from_numpy(rt_pool(5), x)
+        sr.sort(v, key=lambda e: -e)
+        exp = x[np.argsort(-x, kind="stable")]
+        got = v.to_numpy()
+        assert np.array_equal(got, exp)
+        assert np.array_equal(np.signbit(got), np.signbit(exp))
+
 
 class TestAsyncTransfers:
     def test_async_upload_then_compute(self, rt3):
