@@ -601,18 +601,21 @@ def run_e2e(args, rt, world, rank, group, workloads, dt, ngpu=1):
     d2h = (8 if "dot" in sw else 0) + n * 4 * (("triad" in sw) + ("scan" in sw))
 
     def step(i):
+        # c first: the scan needs only c, so its result streams back over PCIe while b is
+        # still uploading (the two directions overlap sooner); dot and triad wait for b.
+        # The three pipelines are independent, so their order inside the step is free.
         a, b, c, o = sets[i % 2]
-        tickets.append(b.upload(hb, wait=False))
         tickets.append(c.upload(hc, wait=False))
+        tickets.append(b.upload(hb, wait=False))
+        if "scan" in sw:
+            spmd.inclusive_scan(c, o, group) if group else A.inclusive_scan(c, o)
+            tickets.append(o.to_numpy(out=ho, wait=False)[1])
         if "dot" in sw:
             z = views.transform(views.zip(b, c), lambda t: t[0] * t[1])
             spmd.reduce(z, 0.0, A.add, group) if group else A.reduce(z, 0.0, A.add)
         if "triad" in sw:
             B.stream_triad(a, b, c)
             tickets.append(a.to_numpy(out=ha, wait=False)[1])
-        if "scan" in sw:
-            spmd.inclusive_scan(c, o, group) if group else A.inclusive_scan(c, o)
-            tickets.append(o.to_numpy(out=ho, wait=False)[1])
 
     def drain():
         for tk in tickets:
