@@ -382,7 +382,12 @@ template <class T, class M = BSMath<T>> struct BlackScholesF {
     T* out;
     const T *S, *K, *r, *v, *t;
   };
-  static constexpr int E = BS_E * 16 / sizeof(T);
+  // the fp32 SFU tier needs ILP (BS_E vectors per thread); the fp64 reference chain is
+  // register-bound, so it runs one vector per thread and more warps
+#ifndef BS_REF_E
+#define BS_REF_E 1
+#endif
+  static constexpr int E = (is_same<M, BSMath<T>>::value ? BS_E : BS_REF_E) * 16 / sizeof(T);
   static constexpr int U = 1;  // transcendental-heavy: fewer registers, more warps
   struct Regs {
     T S[E], K[E], r[E], v[E], t[E];
