@@ -210,6 +210,16 @@ int drk_reduce_batch_ex(int dtype, int op, int nseg, const void* const* xs, cons
 int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
                      void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream);
 int drk_wait_flags(const void* host_flags, int count, uint64_t epoch, int device, void* stream);
+
+/* CUDA graphs of fixed launch sequences (a cached plan that issues several kernels on one
+ * stream): drk_graph_begin starts a thread-local capture on `stream`, the entries called
+ * next are captured instead of run, drk_graph_end instantiates them into *exec (the capture
+ * consumed nothing), drk_graph_launch replays them on a stream of the same device,
+ * drk_graph_destroy frees *exec.  drk_launch_count counts a replay's kernels. */
+int drk_graph_begin(int device, void* stream);
+int drk_graph_end(int device, void* stream, void** exec);
+int drk_graph_launch(void* exec, int device, void* stream);
+int drk_graph_destroy(void* exec);
 /* The batched multi-device variant: every GPU's batched reduction (kind 0) or
  * dot (kind 1) of one algorithm call in one entry.  Segments are listed device by device —
  * counts[d] (1..DRK_RED_SEGS) of them on devices[d] / streams[d] — and device d writes its

@@ -181,7 +181,16 @@ def _run_map_plan(plan, cached=True):
     _finish(rt, launches)
     if bound is None and cached:
         bs = [kernels.bind_map(writes, leaves, length, st) for st, writes, leaves, length in work]
-        plan[2] = bs if all(b is not None for b in bs) else ()  # () = launch through run_map
+        plan[2] = _bind_launches(bs)
+
+
+def _bind_launches(bs):
+    """The fixed-argument launches of a plan: one CUDA graph when several go to one stream,
+    else the BoundMaps; () when any launch needs per-call work (then run_map every time)."""
+    if not bs or not all(b is not None for b in bs):
+        return ()
+    g = kernels.capture(bs) if len(bs) > 1 else None
+    return [g] if g is not None else bs
 
 
 def _collect_writes(result, target, writes):
@@ -1213,7 +1222,7 @@ def copy(src, dst) -> None:
     if bound is None and key is not None:
         bs = [kernels.bind_map([(d, ls.value)], ls.leaves, ls.length, st) if st is not None else None
               for ls, d, st in work]
-        plan[2] = bs if bs and all(b is not None for b in bs) else ()
+        plan[2] = _bind_launches(bs)
 
 
 def _copy_to_host(rt, ls, piece, launches):

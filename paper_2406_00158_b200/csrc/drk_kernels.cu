@@ -814,6 +814,61 @@ extern "C" int drk_reduce_multi(int kind, int dtype, int op, int ndev, const int
   return 0;
 }
 
+// CUDA graphs for launch-bound plans: a cached plan that issues several kernels on one stream
+// (a vector spread over several locales of one GPU) is captured once and replayed with one
+// cudaGraphLaunch.  The capture is thread-local, so other threads' streams are unaffected.
+namespace {
+struct GraphExec {
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;  // kernels in the graph (drk_launch_count accounting per replay)
+  int64_t noted_at_begin = 0;
+};
+thread_local int64_t g_capture_mark = 0;
+}  // namespace
+
+extern "C" int drk_graph_begin(int device, void* stream) {
+  if (int rc = prologue(device, "drk_graph_begin")) return rc;
+  g_capture_mark = drk_launch_count();
+  DRK_CHECK(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return 0;
+}
+
+extern "C" int drk_graph_end(int device, void* stream, void** exec) {
+  if (!exec) return set_error(DRK_E_ARG, "drk_graph_end: null exec");
+  *exec = nullptr;
+  if (int rc = prologue(device, "drk_graph_end")) return rc;
+  cudaGraph_t graph = nullptr;
+  DRK_CHECK(cudaStreamEndCapture((cudaStream_t)stream, &graph));
+  cudaGraphExec_t ge = nullptr;
+  const cudaError_t e = cudaGraphInstantiate(&ge, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGraphInstantiate");
+  GraphExec* g = new GraphExec();
+  g->exec = ge;
+  g->launches = drk_launch_count() - g_capture_mark;
+  // the captured launches did not run: take them back out of the launch count
+  g_launches.fetch_sub(g->launches);
+  *exec = g;
+  return 0;
+}
+
+extern "C" int drk_graph_launch(void* exec, int device, void* stream) {
+  if (!exec) return set_error(DRK_E_ARG, "drk_graph_launch: null exec");
+  if (int rc = prologue(device, "drk_graph_launch")) return rc;
+  GraphExec* g = (GraphExec*)exec;
+  DRK_CHECK(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+  g_launches.fetch_add(g->launches);
+  return 0;
+}
+
+extern "C" int drk_graph_destroy(void* exec) {
+  if (!exec) return 0;
+  GraphExec* g = (GraphExec*)exec;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
+  return 0;
+}
+
 // Host-side wait for completion words written by a kernel into mapped pinned memory: spin
 // (a pause per poll) until every one of `count` words equals `epoch`; the stream is queried
 // every few thousand polls so a failed launch surfaces as its error instead of a hang.

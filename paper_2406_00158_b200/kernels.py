@@ -241,6 +241,65 @@ class BoundMap:
             _lib.check(rc, self.name)
 
 
+class BoundGraph:
+    """Several BoundMaps on one stream captured into one CUDA graph (drk_graph_*): a cached
+    plan over many segments of one GPU replays with a single launch."""
+
+    __slots__ = ("exec", "state", "handles", "keep", "__weakref__")
+
+    def __call__(self):
+        for h in self.handles:
+            if h._pending:
+                from .runtime import await_pending
+
+                await_pending(self.state, self.handles)
+                break
+        rc = _lib.fn("drk_graph_launch")(self.exec, self.state.index, self.state.handle)
+        if rc:
+            _lib.check(rc, "drk_graph_launch")
+
+    def __del__(self):
+        try:
+            if self.exec:
+                _lib.fn("drk_graph_destroy")(self.exec)
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
+
+
+def capture(bounds):
+    """A BoundGraph replaying `bounds` (several BoundMaps of one device state), or None when
+    they do not share a stream or the capture fails (the caller keeps the BoundMaps)."""
+    if len(bounds) < 2 or any(b.state is not bounds[0].state for b in bounds):
+        return None
+    st = bounds[0].state
+    for b in bounds:  # settle pending transfers outside the capture
+        for h in b.handles:
+            if h._pending:
+                from .runtime import await_pending
+
+                await_pending(st, b.handles)
+                break
+    if _lib.fn("drk_graph_begin")(st.index, st.handle):
+        return None
+    ok = True
+    for b in bounds:
+        if b.fn(*b.args):
+            ok = False
+            break
+    ex = ctypes.c_void_p()
+    rc = _lib.fn("drk_graph_end")(st.index, st.handle, ctypes.byref(ex))
+    if not ok or rc or not ex.value:
+        if ex.value:
+            _lib.fn("drk_graph_destroy")(ex)
+        return None
+    g = BoundGraph()
+    g.exec = ex.value
+    g.state = st
+    g.handles = [h for b in bounds for h in b.handles]
+    g.keep = [b.keep for b in bounds]
+    return g
+
+
 def bind_map(writes, leaves, n, state):
     """A BoundMap for run_map(writes, leaves, n) on `state`'s GPU, or None when the launch
     needs per-call work."""
