@@ -211,6 +211,19 @@ int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* con
                      void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream);
 int drk_wait_flags(const void* host_flags, int count, uint64_t epoch, int device, void* stream);
 
+/* drk_reduce_multi with the cross-GPU combine fused into the kernels (the driver's fold,
+ * algorithms.py:146-149, over peer memory): segment k of the listing (device by device, as
+ * drk_reduce_multi) stores its partial into home_slots[slot_of[k]] (8-byte accumulator slots
+ * on devices[0]; an NVLink peer store from the other GPUs), fences system-wide and takes a
+ * ticket on home_counter (4 bytes on devices[0], zero at rest); the CTA with the last ticket
+ * folds every slot in order from init (a drk_partial_dtype value) into result_host_mapped,
+ * re-arms the counter and sets flag_host_mapped (8 bytes) to epoch — wait with
+ * drk_wait_flags(host address of the flag, 1, epoch, ...).  Total segments <= DRK_FOLD_MAX. */
+int drk_reduce_fused(int kind, int dtype, int op, int ndev, const int* devices, void* const* streams,
+                     const int* counts, const void* const* xs, const void* const* ys, const int64_t* ns,
+                     const int* slot_of, void* home_slots, void* home_counter, const void* init,
+                     void* result_host_mapped, void* flag_host_mapped, uint64_t epoch, void* const* scratch);
+
 /* CUDA graphs of fixed launch sequences (a cached plan that issues several kernels on one
  * stream): drk_graph_begin starts a thread-local capture on `stream`, the entries called
  * next are captured instead of run, drk_graph_end instantiates them into *exec (the capture

@@ -85,6 +85,9 @@ SIGNATURES = {
     "drk_dot_batch_ex": (_int, [_int, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), _vp, _vp,
                                 _u64, _vp, _int, _vp]),
     "drk_wait_flags": (_int, [_vp, _int, _u64, _int, _vp]),
+    "drk_reduce_fused": (_int, [_int, _int, _int, _int, ctypes.POINTER(_int), ctypes.POINTER(_vp), ctypes.POINTER(_int),
+                                ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_int),
+                                _vp, _vp, _vp, _vp, _vp, _u64, ctypes.POINTER(_vp)]),
     "drk_graph_begin": (_int, [_int, _vp]),
     "drk_graph_end": (_int, [_int, _vp, ctypes.POINTER(_vp)]),
     "drk_graph_launch": (_int, [_vp, _int, _vp]),

@@ -286,7 +286,7 @@ class _ReducePlan:
     """A reduce over fixed segments: lowered pieces, their launch plan (one batched launch when
     a single GPU holds every piece and the catalogue covers them), and the result decoding."""
 
-    __slots__ = ("rt", "lowered", "op", "opcode", "combiner", "batch", "order", "need")
+    __slots__ = ("rt", "lowered", "op", "opcode", "combiner", "batch", "order", "need", "fused", "dinit")
 
     def __init__(self, rt, pieces, op):
         self.rt = rt
@@ -306,6 +306,8 @@ class _ReducePlan:
             need[id(st)] = (st, need.get(id(st), (st, 0))[1] + 1)
         self.need = list(need.values())
         self.batch = _batch_reduce_plan(rt, lowered, self.opcode) if self.opcode is not None else None
+        self.fused = None  # _FusedReduce, built on first use (reduce_combine="fused")
+        self.dinit = {}    # init -> (P, init as P) of the device folds
 
     def run(self):
         for st, k in self.need:
@@ -369,12 +371,20 @@ class _ReducePlan:
         host fold's bit for bit.  None when the host must fold (see _device_init)."""
         from .runtime import torch
 
-        di = self._device_init(init)
+        k = (type(init), repr(init))
+        di = self.dinit.get(k, 0)
+        if di == 0:
+            di = self._device_init(init)
+            if di is not None:
+                di = (*di, _lib.scalar_buffer(di[1], di[0]))
+            self.dinit[k] = di
         if di is None or len(self.lowered) > _lib.FOLD_MAX:
             return None
-        P, iv = di
+        P, iv, initbuf = di
         rt = self.rt
         mode = rt.reduce_combine
+        if mode == "fused":
+            return self._fused(P, iv, initbuf)
         for st, k in self.need:
             st.ensure_results(k)
         states = sorted(rt.device_states, key=lambda s: s.index)
@@ -425,6 +435,84 @@ class _ReducePlan:
         raw = st0.fetch_host_results(1)
         r = np.frombuffer(raw[: P.itemsize].tobytes(), dtype=P)[0]
         return r.item()
+
+
+    def _fused(self, P, iv, initbuf):
+        """reduce_combine="fused": one drk_reduce_fused call — every GPU's batched kernel stores
+        its segments' partials into slots on the first GPU and the last CTA of the call folds
+        them (segment order, numpy's reduce dtype) straight into mapped host memory.  None
+        (another mode runs) when the pieces are not a catalogue batch."""
+        fp = self.fused
+        if fp is None:
+            fp = self.fused = _FusedReduce.build(self) or False
+        if fp is False:
+            return None
+        return fp.run(P, iv, initbuf)
+
+
+class _FusedReduce:
+    """The fixed arguments of a drk_reduce_fused call for one reduce plan (built once)."""
+
+    __slots__ = ("home", "states", "handles", "args_head", "args_tail", "total", "scratch")
+
+    @staticmethod
+    def build(plan):
+        rt = plan.rt
+        st_of = [rt.state_of(lw.rank if lw.rank is not None else 0) for lw in plan.lowered]
+        groups = {}
+        for j, st in enumerate(st_of):
+            groups.setdefault(id(st), (st, []))[1].append(j)
+        gs = sorted(groups.values(), key=lambda g: g[0].index)
+        if any(len(ix) > _lib.RED_SEGS for _, ix in gs) or len(plan.lowered) > _lib.FOLD_MAX:
+            return None
+        plans_ = [kernels.catalogue_reduce(lw.value, lw.leaves, plan.opcode, st.index)
+                  for lw, st in zip(plan.lowered, st_of)]
+        if any(p is None for p in plans_) or len({(p[0], p[1]) for p in plans_}) != 1:
+            return None
+        f = _FusedReduce()
+        f.home = gs[0][0]
+        f.states = [st for st, _ in gs]
+        f.handles = [(st, [lf.handle for j in ix for lf in plan.lowered[j].leaves if lf.handle is not None])
+                     for st, ix in gs]
+        total = f.total = len(plan.lowered)
+        flat = [j for _, ix in gs for j in ix]
+        nd, vp = len(gs), ctypes.c_void_p
+        kind, code = plans_[0][0], plans_[0][1]
+        buf = f.home.combine_slots(8 * _lib.FOLD_MAX + 64)
+        f.args_head = (0 if kind == "reduce" else 1, code, plan.opcode, nd,
+                       (ctypes.c_int * nd)(*[st.index for st in f.states]),
+                       (vp * nd)(*[st.handle for st in f.states]),
+                       (ctypes.c_int * nd)(*[len(ix) for _, ix in gs]),
+                       (vp * total)(*[plans_[j][2] for j in flat]),
+                       (vp * total)(*[plans_[j][3] for j in flat]) if kind == "dot" else None,
+                       (ctypes.c_int64 * total)(*[plan.lowered[j].length for j in flat]),
+                       (ctypes.c_int * total)(*flat), buf.data_ptr(), buf.data_ptr() + 8 * _lib.FOLD_MAX)
+        f.args_tail = [len(ix) for _, ix in gs]
+        f.scratch = None
+        return f
+
+    def run(self, P, iv, initbuf):
+        from .runtime import _EPOCHS, await_pending
+
+        for st, hs in self.handles:
+            for h in hs:
+                if h._pending:
+                    await_pending(st, hs)
+                    break
+        home = self.home
+        fh, fd = home.flag_ptrs()
+        epoch = next(_EPOCHS)
+        bufs = [st.reduce_batch_scratch(c) for st, c in zip(self.states, self.args_tail)]
+        if self.scratch is None or any(a is not b for a, b in zip(bufs, self.scratch[0])):
+            self.scratch = (bufs, (ctypes.c_void_p * len(bufs))(*[b.data_ptr() for b in bufs]))
+        rc = _lib.fn("drk_reduce_fused")(*self.args_head, ctypes.addressof(initbuf), home.host_result_dev_ptr(0),
+                                         fd, epoch, self.scratch[1])
+        if rc:
+            _lib.check(rc, "drk_reduce_fused")
+        rc = _lib.fn("drk_wait_flags")(fh, 1, epoch, home.index, home.handle)
+        if rc:
+            _lib.check(rc, "drk_wait_flags")
+        return np.frombuffer(home._host_results_np, dtype=P, count=1)[0].item()
 
 
 def _segment_partials(rt, pieces, op):

@@ -90,12 +90,6 @@ struct FoldArgs {
   const void* part[DRK_FOLD_MAX];
 };
 
-// numpy's reduce dtype P of a value dtype T (float32 stays float32, int32 sums / products
-// widen to int64 = the accumulator): the dtype the reference's driver folds in
-template <class T, class Op> struct PartialOf {
-  typedef typename std::conditional<is_float<T>::value, T, typename WideAcc<T, Op>::type>::type type;
-};
-
 // acc = init; acc = acc ⊕ P(partial_k) for k = 0..count-1, in P (one thread: count <= 64)
 template <class T, class Op>
 __global__ void reduce_fold_kernel(const FoldArgs a, int count, typename PartialOf<T, Op>::type init,

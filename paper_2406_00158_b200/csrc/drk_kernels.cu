@@ -682,10 +682,22 @@ extern "C" int drk_reduce(int dtype, int op, const void* x, int64_t n, void* res
 // one wave of CTAs is split between the segments in proportion to their lengths, and each
 // segment folds its own CTA partials (same determinism as drk_reduce).  `results` gets one
 // 8-byte slot per segment, `scratch` nseg x drk_reduce_scratch_bytes().
+// the fused cross-GPU combine of one call (FusedCombine in drk_device.cuh), host side
+struct FusedSpec {
+  void* slots;
+  u32* counter;
+  u32 total;
+  u64 init_bits;
+  void* result;
+  u64* flag;
+  u64 epoch;
+  const int* gslot;  // global slot of each of this launch's segments
+};
+
 template <class LD, class Op>
 static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const int64_t* ns, const bool* vec_ok,
                                void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream,
-                               const char* what) {
+                               const char* what, const FusedSpec* fs = nullptr) {
   typedef typename WideAcc<typename LD::V, Op>::type A;
   if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, std::string(what) + ": nseg out of range");
   if (!results || !scratch) return set_error(DRK_E_ARG, std::string(what) + ": null results/scratch");
@@ -718,8 +730,19 @@ static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const in
     b.s[k] = carve_reduce((char*)scratch + (size_t)k * sbytes);
     b.result[k] = (A*)((char*)results + 8 * (size_t)k);
     b.flag[k] = flags ? (u64*)flags + k : nullptr;
+    if (fs) b.gslot[k] = (u32)fs->gslot[k];
   }
   b.epoch = epoch;
+  if (fs) {
+    b.fused = 1;
+    b.fc.slots = (A*)fs->slots;
+    b.fc.counter = fs->counter;
+    b.fc.total = fs->total;
+    b.fc.init_bits = fs->init_bits;
+    b.fc.result = fs->result;
+    b.fc.flag = fs->flag;
+    b.fc.epoch = fs->epoch;
+  }
   b.cta_first[nseg] = first;
   kern<<<first, BLOCK, 0, (cudaStream_t)stream>>>(b);
   return epilogue(what);
@@ -727,7 +750,7 @@ static int launch_reduce_batch(int nseg, const typename LD::Params* ps, const in
 
 template <class T>
 static int reduce_batch_op(int op, int nseg, const void* const* xs, const int64_t* ns, void* results, void* flags,
-                           uint64_t epoch, void* scratch, int device, void* stream) {
+                           uint64_t epoch, void* scratch, int device, void* stream, const FusedSpec* fs = nullptr) {
   typename IdentLoad<T>::Params ps[DRK_RED_SEGS];
   bool v[DRK_RED_SEGS];
   if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_reduce_batch: nseg out of range");
@@ -738,10 +761,10 @@ static int reduce_batch_op(int op, int nseg, const void* const* xs, const int64_
   }
   const char* w = "drk_reduce_batch";
   switch (op) {
-    case DRK_ADD: return launch_reduce_batch<IdentLoad<T>, OpAdd>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
-    case DRK_MUL: return launch_reduce_batch<IdentLoad<T>, OpMul>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
-    case DRK_MIN: return launch_reduce_batch<IdentLoad<T>, OpMin>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
-    case DRK_MAX: return launch_reduce_batch<IdentLoad<T>, OpMax>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w);
+    case DRK_ADD: return launch_reduce_batch<IdentLoad<T>, OpAdd>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w, fs);
+    case DRK_MUL: return launch_reduce_batch<IdentLoad<T>, OpMul>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w, fs);
+    case DRK_MIN: return launch_reduce_batch<IdentLoad<T>, OpMin>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w, fs);
+    case DRK_MAX: return launch_reduce_batch<IdentLoad<T>, OpMax>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream, w, fs);
   }
   return set_error(DRK_E_ARG, "drk_reduce_batch: unknown op");
 }
@@ -759,8 +782,9 @@ extern "C" int drk_reduce_batch(int dtype, int op, int nseg, const void* const* 
   return drk_reduce_batch_ex(dtype, op, nseg, xs, ns, results, nullptr, 0, scratch, device, stream);
 }
 
-extern "C" int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
-                                void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream) {
+static int dot_batch_any(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                         void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream,
+                         const FusedSpec* fs) {
   if (!xs || !ys || !ns) return set_error(DRK_E_ARG, "drk_dot_batch: null segment arrays");
   if (nseg < 1 || nseg > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_dot_batch: nseg out of range");
   DRK_DISPATCH(dtype, "drk_dot_batch", T, {
@@ -772,8 +796,13 @@ extern "C" int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, cons
       v[k] = aligned16(xs[k]) && aligned16(ys[k]);
     }
     return launch_reduce_batch<ProdLoad<T>, OpAdd>(nseg, ps, ns, v, results, flags, epoch, scratch, device, stream,
-                                                  "drk_dot_batch");
+                                                  "drk_dot_batch", fs);
   });
+}
+
+extern "C" int drk_dot_batch_ex(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
+                                void* results, void* flags, uint64_t epoch, void* scratch, int device, void* stream) {
+  return dot_batch_any(dtype, nseg, xs, ys, ns, results, flags, epoch, scratch, device, stream, nullptr);
 }
 
 extern "C" int drk_dot_batch(int dtype, int nseg, const void* const* xs, const void* const* ys, const int64_t* ns,
@@ -866,6 +895,62 @@ extern "C" int drk_graph_destroy(void* exec) {
   GraphExec* g = (GraphExec*)exec;
   if (g->exec) cudaGraphExecDestroy(g->exec);
   delete g;
+  return 0;
+}
+
+// drk_reduce_multi with the cross-GPU combine fused into the kernels (FusedCombine): segment k
+// of the listing stores its partial into home_slots[slot_of[k]] (8-byte slots on devices[0],
+// peer memory for the others), and the last CTA of the call folds them in slot order from
+// init (partial dtype) into result_host_mapped and sets flag_host_mapped to epoch.  One wait
+// on one word, no fold on the host.  home_counter (4 bytes on devices[0]) must be zero.
+extern "C" int drk_reduce_fused(int kind, int dtype, int op, int ndev, const int* devices, void* const* streams,
+                                const int* counts, const void* const* xs, const void* const* ys, const int64_t* ns,
+                                const int* slot_of, void* home_slots, void* home_counter, const void* init,
+                                void* result_host_mapped, void* flag_host_mapped, uint64_t epoch,
+                                void* const* scratch) {
+  if (kind != 0 && kind != 1) return set_error(DRK_E_ARG, "drk_reduce_fused: kind must be 0 (reduce) or 1 (dot)");
+  if (ndev < 1 || !devices || !streams || !counts || !xs || !ns || !slot_of || !home_slots || !home_counter ||
+      !init || !result_host_mapped || !flag_host_mapped || !scratch || (kind == 1 && !ys))
+    return set_error(DRK_E_ARG, "drk_reduce_fused: null argument");
+  int total = 0;
+  for (int d = 0; d < ndev; ++d) {
+    if (counts[d] < 1 || counts[d] > DRK_RED_SEGS) return set_error(DRK_E_ARG, "drk_reduce_fused: count out of range");
+    if (!scratch[d]) return set_error(DRK_E_ARG, "drk_reduce_fused: null scratch");
+    total += counts[d];
+  }
+  if (total > DRK_FOLD_MAX) return set_error(DRK_E_ARG, "drk_reduce_fused: more than DRK_FOLD_MAX segments");
+  for (int k = 0; k < total; ++k) {
+    if (slot_of[k] < 0 || slot_of[k] >= total) return set_error(DRK_E_ARG, "drk_reduce_fused: slot out of range");
+    if (!xs[k] || (kind == 1 && !ys[k]) || ns[k] < 1) return set_error(DRK_E_ARG, "drk_reduce_fused: bad segment");
+  }
+  const int pd = drk_partial_dtype(dtype, op);
+  if (pd < 0) return set_error(DRK_E_DTYPE, "drk_reduce_fused: unknown dtype");
+  FusedSpec fs;
+  fs.slots = home_slots;
+  fs.counter = (u32*)home_counter;
+  fs.total = (u32)total;
+  fs.init_bits = 0;
+  memcpy(&fs.init_bits, init, (pd == DRK_F32 || pd == DRK_I32) ? 4 : 8);
+  fs.result = result_host_mapped;
+  fs.flag = (u64*)flag_host_mapped;
+  fs.epoch = epoch;
+  int off = 0;
+  for (int d = 0; d < ndev; ++d) {
+    fs.gslot = slot_of + off;
+    int rc;
+    if (kind == 0) {
+      DRK_DISPATCH(dtype, "drk_reduce_fused", T, {
+        rc = reduce_batch_op<T>(op, counts[d], xs + off, ns + off, home_slots, nullptr, 0, scratch[d], devices[d],
+                                streams[d], &fs);
+        break;
+      });
+    } else {
+      rc = dot_batch_any(dtype, counts[d], xs + off, ys + off, ns + off, home_slots, nullptr, 0, scratch[d],
+                         devices[d], streams[d], &fs);
+    }
+    if (rc) return rc;
+    off += counts[d];
+  }
   return 0;
 }
 

@@ -78,7 +78,10 @@ class AggregateTaskError(RuntimeError):
 # host folds them; "device" — the first GPU folds them from peer memory (NVLink) and stores
 # one result; "nccl" — an NCCL all-gather of the partials, then every GPU folds them in
 # segment order (all-reduce semantics, the result on every GPU).  Same value every way.
-REDUCE_COMBINES = ("host", "device", "nccl")
+# "fused" — the combine inside the reduce kernels: each segment's partial goes into a slot on
+# the first GPU (NVLink peer stores), and the kernel CTA that finishes last folds them and
+# stores the result into mapped host memory (drk_reduce_fused): one kernel per GPU, one wait.
+REDUCE_COMBINES = ("host", "device", "nccl", "fused")
 
 _EPOCHS = itertools.count(1)  # completion-word epochs (DeviceState.completion_flags)
 

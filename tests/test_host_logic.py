@@ -220,7 +220,7 @@ def test_reduce_combine_option():
     import paper_2406_00158_b200 as sr
     from paper_2406_00158_b200.runtime import REDUCE_COMBINES
 
-    assert REDUCE_COMBINES == ("host", "device", "nccl")
+    assert REDUCE_COMBINES == ("host", "device", "nccl", "fused")
     for mode in REDUCE_COMBINES:
         assert sr.Runtime(2, backend="meta", reduce_combine=mode).reduce_combine == mode
     assert sr.Runtime(2, backend="meta").reduce_combine in REDUCE_COMBINES

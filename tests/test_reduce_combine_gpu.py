@@ -1,4 +1,5 @@
-"""Cross-GPU combine of reduce on the device (Runtime(reduce_combine="device" | "nccl")).
+"""Cross-GPU combine of reduce on the device (Runtime(reduce_combine="device" | "nccl" |
+"fused")).
 
 The reference folds per-segment partials on the driver in ascending order
 (algorithms.py:146-149).  The device folds (drk_reduce_fold from peer memory, and the NCCL
@@ -22,7 +23,7 @@ pytestmark = pytest.mark.gpu
 
 CASES = golden().cases
 REL = {"float32": 1e-5, "float64": 1e-12}
-MODES = ("device", "nccl")
+MODES = ("device", "nccl", "fused")
 
 
 def _close(got, exp, dtype):

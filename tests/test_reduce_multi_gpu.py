@@ -15,9 +15,9 @@ from oracle import segrange_port as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def split_rt(monkeypatch):
-    rt = sr.Runtime(5, devices=[0])
+@pytest.fixture(params=["host", "fused"])
+def split_rt(monkeypatch, request):
+    rt = sr.Runtime(5, devices=[0], reduce_combine=request.param)
     alt = DeviceState(0, "cuda")
     orig = rt.state_of
     monkeypatch.setattr(rt, "state_of", lambda loc: alt if loc % 2 else orig(loc))
@@ -38,7 +38,7 @@ def test_reduce_multi_matches_oracle(split_rt, dtype):
     x = O.mod_ints(7, 0, n, 2001, -1000).astype(dtype)
     v = sr.DistributedVector.from_numpy(rt, x)
     rt.synchronize()
-    assert isinstance(_plan(rt, v).batch, A._MultiReduce)
+    assert isinstance(_plan(rt, v).batch, A._MultiReduce)  # host mode runs it; fused mode folds in-kernel
     got = A.reduce(v, 0, A.add)
     want = O.reduce(x, 5, 0)
     assert type(got) is type(want)

@@ -19,7 +19,7 @@ def per_call(f, reps):
     return (time.perf_counter() - t0) / reps * 1e6
 
 
-for mode in ("host", "device", "nccl"):
+for mode in ("host", "device", "nccl", "fused"):
     rt = sr.Runtime(2, reduce_combine=mode)
     n = 1 << 24
     x = sr.DistributedVector(rt, n, dtype=np.float32)
