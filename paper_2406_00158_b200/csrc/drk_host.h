@@ -33,7 +33,7 @@ static constexpr int MAX_RED_GRID = 4096;
 extern std::mutex g_mu;
 extern int g_map_waves;     // 0: size grid to cover the work once (non-persistent)
 extern int g_reduce_waves;  // reduce grid = SMs * occupancy * waves
-extern int g_scan_sub;      // scan sub-tiles per CTA tile (1..4)
+extern int g_scan_sub;      // scan sub-tiles per CTA tile (1..4; 0: by size)
 extern int g_scan_l2dyn;    // L2-resident two-touch scan for large aligned segments
 extern int g_scan_l2_min;
 extern int g_scan_l2_subs;  // sub-tiles per L2 tile (0: 8 = 160 KB for 4-byte types)

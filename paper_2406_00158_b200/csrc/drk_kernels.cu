@@ -141,7 +141,7 @@ std::mutex g_mu;
 int g_map_waves = 0;
 int g_reduce_waves = 1;
 int g_reduce_grid = 0;  // experiments: cap on the reduce grid (0: SMs x occupancy x waves)
-int g_scan_sub = 3;
+int g_scan_sub = 0;  // 0: by segment size (drk_scan.cu)
 int g_scan_l2dyn = 1;
 int g_scan_l2_min = 1 << 22;
 int g_scan_l2_subs = 0;
@@ -243,7 +243,7 @@ extern "C" int drk_tune(const char* name, int value) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)value << 20);
   } else if (!strcmp(name, "scan_sub")) {
     old = g_scan_sub;
-    if (value >= 1 && value <= 4) g_scan_sub = value;
+    if (value >= 0 && value <= 4) g_scan_sub = value;
   }
   return old;
 }
