@@ -617,9 +617,23 @@ class _MultiReduce:
         flags = (vp * nd)(*[p[1] for p in ptrs])
         scratch = (vp * nd)(*[st.reduce_batch_scratch(c).data_ptr() for st, c in zip(self.states, self.counts)])
         epoch = next(_EPOCHS)
-        _lib.call("drk_reduce_multi", 0 if self.kind == "reduce" else 1, self.code, self.opcode, nd, self.devices,
-                  self.streams, (ctypes.c_int * nd)(*self.counts), self.xs, self.ys, self.ns, results, flags, epoch,
-                  scratch)
+        if kernels._PROFILE is None:
+            _lib.call("drk_reduce_multi", 0 if self.kind == "reduce" else 1, self.code, self.opcode, nd, self.devices,
+                      self.streams, (ctypes.c_int * nd)(*self.counts), self.xs, self.ys, self.ns, results, flags,
+                      epoch, scratch)
+        else:  # profiled runs (bench.py): each GPU's batched launch, timed on its own stream
+            off = 0
+            for d, (st, c) in enumerate(zip(self.states, self.counts)):
+                xs = (vp * c)(*self.xs[off:off + c])
+                ns = (ctypes.c_int64 * c)(*self.ns[off:off + c])
+                if self.kind == "reduce":
+                    kernels.launch_kernel("drk_reduce_batch_ex", Launch(st), sum(ns), self.code, self.opcode, c, xs,
+                                          ns, results[d], flags[d], epoch, scratch[d])
+                else:
+                    ys = (vp * c)(*self.ys[off:off + c])
+                    kernels.launch_kernel("drk_dot_batch_ex", Launch(st), sum(ns), self.code, c, xs, ys, ns,
+                                          results[d], flags[d], epoch, scratch[d])
+                off += c
         out = [None] * sum(self.counts)
         for st, c, (fh, _), fmt, dec, ix in zip(self.states, self.counts, ptrs, self.fmts, self.decode, self.order):
             _lib.call("drk_wait_flags", fh, c, epoch, st.index, st.handle)

@@ -62,3 +62,21 @@ def test_dot_multi_matches_oracle(split_rt):
     assert abs(got - want) <= 1e-5 * abs(want)
     for _ in range(3):  # the cached plan, repeated (fresh epochs each call)
         assert B.dot_product(vx, vy) == got
+
+
+def test_multi_reduce_under_profile(split_rt):
+    """bench.py times kernels with kernels.profile(): the multi-device reduce then launches
+    each GPU's batch through the profiler (both launches recorded), with the same result."""
+    from paper_2406_00158_b200 import kernels
+
+    rt = split_rt
+    if rt.reduce_combine != "host":
+        pytest.skip("the profiled multi-device launch is the host-combine path")
+    x = O.mod_ints(9, 0, 100_003, 2001, -1000).astype(np.int64)
+    v = sr.DistributedVector.from_numpy(rt, x)
+    rt.synchronize()
+    want = A.reduce(v, 0, A.add)
+    with kernels.profile() as prof:
+        got = A.reduce(v, 0, A.add)
+    assert got == want == int(x.sum())
+    assert len(prof.records.get("drk_reduce_batch", [])) == 2
