@@ -65,3 +65,33 @@ def test_zero_length_is_a_no_op():
 
 def test_device_count_is_zero_or_more():
     assert _lib.device_count() >= 0
+
+
+def test_round2_entries_validate_before_any_launch():
+    """The round-2 entries (multi-device / fused reduce, device fold, communicator, graphs,
+    completion words, Black-Scholes tiers) reject bad arguments before touching a device."""
+    lib = _lib.load()
+    vp = ctypes.c_void_p
+    one = (ctypes.c_int * 1)(1)
+    assert lib.drk_reduce_multi(5, _lib.F32, _lib.ADD, 1, one, (vp * 1)(), one, (vp * 1)(), None,
+                                (ctypes.c_int64 * 1)(4), (vp * 1)(), None, 1, (vp * 1)()) == _lib.E_ARG
+    assert "kind" in _lib.last_error()
+    assert lib.drk_reduce_multi(0, _lib.F32, _lib.ADD, 1, one, (vp * 1)(), (ctypes.c_int * 1)(17), (vp * 1)(),
+                                None, (ctypes.c_int64 * 1)(4), (vp * 1)(1), None, 1, (vp * 1)(1)) == _lib.E_ARG
+    assert lib.drk_reduce_fused(0, _lib.F32, _lib.ADD, 1, one, (vp * 1)(), one, (vp * 1)(), None,
+                                (ctypes.c_int64 * 1)(4), (ctypes.c_int * 1)(0), None, None, None, None, None, 1,
+                                (vp * 1)()) == _lib.E_ARG
+    assert lib.drk_reduce_fold(_lib.F32, _lib.ADD, None, _lib.FOLD_MAX + 1, None, None, None, 0, None) == _lib.E_ARG
+    h = ctypes.c_void_p()
+    assert lib.drk_comm_create(0, None, ctypes.byref(h)) == _lib.E_ARG
+    assert lib.drk_comm_create(2, (ctypes.c_int * 2)(0, 0), ctypes.byref(h)) == _lib.E_ARG
+    assert "duplicate" in _lib.last_error()
+    assert lib.drk_graph_launch(None, 0, None) == _lib.E_ARG
+    assert lib.drk_graph_destroy(None) == 0
+    assert lib.drk_wait_flags(None, 1, 1, 0, None) == _lib.E_ARG
+    assert lib.drk_wait_flags(None, 0, 1, 0, None) == 0
+    assert lib.drk_black_scholes_ex(_lib.F32, 4, 1, 1, 1, 1, 1, 1, 16, 0, None) == _lib.E_ARG
+    assert "flags" in _lib.last_error()
+    assert lib.drk_partial_dtype(_lib.F32, _lib.ADD) == _lib.F32
+    assert lib.drk_partial_dtype(_lib.I32, _lib.ADD) == _lib.I64
+    assert lib.drk_partial_dtype(_lib.I32, _lib.MIN) == _lib.I32

@@ -126,3 +126,14 @@ def test_nccl_allgather_one_rank(pools):
               (vp * 1)(st.handle))
     st.synchronize()
     assert torch.equal(src, dst)
+
+
+def test_wait_flags_reports_a_missing_completion(pools):
+    """drk_wait_flags on an idle stream whose completion word never arrives returns an error
+    instead of spinning forever."""
+    rt = pools("host", 2)
+    st = rt.device_states[0]
+    fh, _ = st.flag_ptrs()
+    st.synchronize()
+    rc = _lib.load().drk_wait_flags(fh, 1, (1 << 62) + 12345, st.index, st.handle)
+    assert rc == _lib.E_ARG and "idle" in _lib.last_error()
