@@ -305,3 +305,151 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
         return carry_ptr, host_value
 
     return hook
+
+
+# ----------------------------------------------------------------------------------------
+# distributed sample sort, one process per GPU (reference algorithms.py:315-432)
+
+
+def _exchange(send, sizes_out, sizes_in, group: Group, st):
+    """all-to-all-v of a 1-D device tensor's bytes: sizes_out[j] bytes (consecutive) to rank
+    j, sizes_in[j] from rank j, in rank order.  NCCL runs on the rank's stream (NVLink);
+    gloo (the shared-GPU test mode) stages through host memory."""
+    t = _torch()
+    dist = _dist()
+    total_in = int(sum(sizes_in))
+    src = send.view(t.uint8) if send.numel() else send.new_empty(0, dtype=t.uint8)
+    if group.backend == "nccl":
+        with t.cuda.device(st.index), t.cuda.stream(st.stream):
+            out = t.empty(total_in, dtype=t.uint8, device=st.device)
+            dist.all_to_all_single(out, src, [int(s) for s in sizes_in], [int(s) for s in sizes_out],
+                                   group=group.group)
+        return out
+    st.synchronize()
+    host_in = src.cpu()
+    host_out = t.empty(total_in, dtype=t.uint8)
+    dist.all_to_all_single(host_out, host_in, [int(s) for s in sizes_in], [int(s) for s in sizes_out],
+                           group=group.group)
+    with t.cuda.stream(st.stream):
+        return host_out.to(st.device, non_blocking=False)
+
+
+def sort(local, group: Group, key=None) -> None:
+    """Sort the global vector whose block r is rank r's `local` DistributedVector, in place,
+    ascending (by key if given, stably): after the call rank r's block holds sorted positions
+    [offset_r, offset_r + len(local)) — the reference's sample sort with one segment per rank:
+      1. the rank's elements sorted on its GPU (the library's radix sort; key functions run on
+         the device and the elements follow a stable pair sort);
+      2. P-1 evenly spaced samples per rank, all-gathered; splitters picked from the pool like
+         the reference's driver (algorithms.py:358-367);
+      3. counts of the rank's run per destination (drk_sort_bounds) all-gathered;
+      4. one all-to-all-v moves the runs (NCCL over NVLink), a stable sort of the received
+         chunk (runs arrive in rank order, so ties keep their global order);
+      5. a second all-to-all-v restores every rank's length (the reference's sweep back).
+    Every rank must call it (a collective)."""
+    from . import _sort as S
+    from . import algorithms as A
+    from . import kernels
+    from .runtime import await_pending, torch_dtype
+
+    t = _torch()
+    dist = _dist()
+    P, r = group.size, group.rank
+    rt = A.runtime_of(local)
+    segs = A.segments_of(local)
+    for s in segs:
+        if not hasattr(s, "handle"):
+            raise TypeError("sort needs raw writable storage segments")
+    live = [s for s in segs if len(s)]
+    T = np.dtype(local.dtype)
+    vcode = _lib.sort_dtype_code(T)
+    states = {rt.state_of(s.rank).index for s in segs}
+    if len(states) > 1:
+        raise ValueError("spmd.sort: a rank's segments must live on one GPU")
+    st = rt.state_of(segs[0].rank)
+    for s in live:
+        await_pending(st, [s.handle])
+    n_r = sum(len(s) for s in segs)
+    # the rank's block as one device buffer
+    with t.cuda.stream(st.stream):
+        vals = t.empty(n_r, dtype=torch_dtype(T), device=st.device)
+    pos = 0
+    for s in live:
+        _lib.call("drk_memcpy_async", vals.data_ptr() + pos * T.itemsize,
+                  s.handle.data_ptr() + s.start * T.itemsize, len(s) * T.itemsize, st.index, st.handle)
+        pos += len(s)
+    node, K = (S._key_node(key, T) if key is not None else (None, T))
+    kcode = _lib.sort_dtype_code(K)
+    keep = []
+
+    def keys_of(v, m):
+        """Device keys of the m elements of v (the values themselves without a key)."""
+        if node is None:
+            return v
+        from .algorithms import _DeviceTarget
+
+        with t.cuda.stream(st.stream):
+            k = t.empty(m, dtype=torch_dtype(K), device=st.device)
+        if m:
+            kernels.run_map([(_DeviceTarget(k, K, st.index), node)], [kernels._TensorLeaf(v, T, m)], m,
+                            kernels.Launch(st))
+        return k
+
+    def local_sort(v, m):
+        k = keys_of(v, m)
+        if m > 1:
+            keep.extend(S._sort_buffer(st, kcode, k, m, None if node is None else v, vcode))
+        return k
+
+    # 1. local sort
+    keys = local_sort(vals, n_r)
+    # 2. samples -> splitters
+    spos = S._sorted_positions(n_r, P)
+    if spos:
+        with t.cuda.stream(st.stream):
+            idx = t.tensor(spos, dtype=t.int64).to(st.device)
+            smp = keys[idx]
+        st.synchronize()
+        samples = smp.cpu().numpy()
+    else:
+        samples = np.empty(0, dtype=K)
+    pools = [None] * P
+    dist.all_gather_object(pools, samples, group=group.group)
+    pool = np.concatenate([p for p in pools if len(p)]) if any(len(p) for p in pools) else np.empty(0, dtype=K)
+    pool = pool[np.argsort(pool, kind="stable")]
+    m = len(pool)
+    split = np.ascontiguousarray(pool[[(j + 1) * m // P for j in range(P - 1)]]) if m else np.empty(0, dtype=K)
+    # 3. counts of this run per destination
+    if P > 1 and n_r and len(split) == P - 1:
+        with t.cuda.stream(st.stream):
+            split_d = t.from_numpy(split).to(st.device, non_blocking=False)
+            bnd = t.empty(P - 1, dtype=t.int64, device=st.device)
+        _lib.call("drk_sort_bounds", kcode, keys.data_ptr(), n_r, split_d.data_ptr(), P - 1, bnd.data_ptr(),
+                  st.index, st.handle)
+        st.synchronize()
+        counts = np.diff(np.concatenate(([0], bnd.cpu().numpy(), [n_r])))
+    else:
+        counts = np.zeros(P, dtype=np.int64)
+        counts[min(r, P - 1) if not len(split) else 0] = n_r
+    table = [None] * P
+    dist.all_gather_object(table, (n_r, counts.astype(np.int64)), group=group.group)
+    lens = np.array([x[0] for x in table], dtype=np.int64)
+    cmat = np.stack([x[1] for x in table])          # cmat[k][j]: rank k's elements for chunk j
+    # 4. the runs to their chunks, then a stable chunk sort
+    chunk = _exchange(vals, counts * T.itemsize, cmat[:, r] * T.itemsize, group, st).view(torch_dtype(T))
+    S_r = int(cmat[:, r].sum())
+    local_sort(chunk, S_r)
+    # 5. back to every rank's own length: chunk r covers global [C_r, C_r + S_r)
+    sizes = cmat.sum(axis=0)
+    C = np.concatenate(([0], np.cumsum(sizes)))
+    off = np.concatenate(([0], np.cumsum(lens)))
+    send = [max(0, min(C[r + 1], off[q + 1]) - max(C[r], off[q])) for q in range(P)]
+    recv = [max(0, min(C[q + 1], off[r + 1]) - max(C[q], off[r])) for q in range(P)]
+    result = _exchange(chunk, np.array(send) * T.itemsize, np.array(recv) * T.itemsize, group, st)
+    pos = 0
+    for s in live:
+        _lib.call("drk_memcpy_async", s.handle.data_ptr() + s.start * T.itemsize,
+                  result.data_ptr() + pos * T.itemsize, len(s) * T.itemsize, st.index, st.handle)
+        pos += len(s)
+    st.synchronize()
+    del keep

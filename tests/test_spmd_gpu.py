@@ -1,6 +1,6 @@
 """The one-process-per-GPU path (spmd.py + bench.py under torchrun) on a single GPU:
 three ranks share GPU 0 and exchange over gloo (NCCL refuses two ranks on one device).
-Checks distributed dot / inclusive and exclusive scan / min against numpy."""
+Checks distributed dot / inclusive and exclusive scan / min / sample sort against numpy."""
 
 import os
 import socket
@@ -26,7 +26,8 @@ def test_spmd_three_ranks_one_gpu():
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "spmd_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    assert out.stdout.count("'dot': True, 'scan': True, 'exscan': True, 'min': True") == 3
+    assert out.stdout.count("'dot': True, 'scan': True, 'exscan': True, 'min': True, 'sort': True, "
+                            "'keysort': True") == 3
 
 
 def test_spmd_nccl_one_rank():
@@ -37,7 +38,7 @@ def test_spmd_nccl_one_rank():
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "spmd_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    assert "'dot': True, 'scan': True, 'exscan': True, 'min': True" in out.stdout
+    assert "'dot': True, 'scan': True, 'exscan': True, 'min': True, 'sort': True, 'keysort': True" in out.stdout
 
 
 def test_bench_two_ranks_shared_gpu():

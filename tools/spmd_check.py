@@ -1,5 +1,6 @@
 """Multi-process check of the one-process-per-GPU path on a single GPU (gloo exchange,
-all ranks on GPU 0): distributed dot and scan of a global vector against numpy.
+all ranks on GPU 0): distributed dot, scans, min and sample sort of a global vector against
+numpy.
 SPMD_BACKEND=nccl (one rank) runs the NCCL exchange: kernel-built pairs, all-gather on the
 compute stream, kernel readback."""
 import os, sys
@@ -36,6 +37,21 @@ ok = {
     "exscan": bool(np.array_equal(outx.to_numpy(), (7 + np.concatenate([[0], inc[:-1]]))[rank * n:(rank + 1) * n].astype(np.int32))),
     "min": mn == int(gi.min()),
 }
+# distributed sample sort (spmd.sort): uneven blocks, float64 with NaNs, and a keyed stable sort
+lens = [50_000 + 997 * q for q in range(world)]
+offs = np.concatenate([[0], np.cumsum(lens)])
+gf = O.unit_doubles(8, 0, int(offs[-1])) * 100.0
+gf[::97] = np.nan
+gf[5::13] = 42.0
+vf = sr.DistributedVector.from_numpy(rt, gf[offs[rank]:offs[rank + 1]])
+spmd.sort(vf, g)
+gk = O.mod_ints(9, 0, int(offs[-1]), 1001, -500).astype(np.int64)
+vk = sr.DistributedVector.from_numpy(rt, gk[offs[rank]:offs[rank + 1]])
+spmd.sort(vk, g, key=lambda e: e % 7)
+got = [None] * world
+dist.all_gather_object(got, (vf.to_numpy(), vk.to_numpy()))
+ok["sort"] = bool(np.array_equal(np.concatenate([a for a, _ in got]), np.sort(gf), equal_nan=True))
+ok["keysort"] = bool(np.array_equal(np.concatenate([b for _, b in got]), gk[np.argsort(gk % 7, kind="stable")]))
 print(f"rank {rank}/{world}: {ok}", flush=True)
 dist.destroy_process_group()
 sys.exit(0 if all(ok.values()) else 1)
