@@ -151,7 +151,6 @@ int g_scan_debug = 0;
 int g_scan_stagger = -1;
 int g_scan_smem_pad = 0;
 int g_scan_rescan_pol = 0;
-int g_scan_exp = 0;
 int g_scan_keep_tail = 1;
 thread_local int g_chain_launch = 0;
 void* g_scan_trace = nullptr;
@@ -229,9 +228,6 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_keep_tail")) {
     old = g_scan_keep_tail;
     g_scan_keep_tail = value;
-  } else if (!strcmp(name, "scan_exp")) {
-    old = g_scan_exp;
-    g_scan_exp = value;
   } else if (!strcmp(name, "scan_rescan_pol")) {
     old = g_scan_rescan_pol;
     g_scan_rescan_pol = value;

@@ -64,20 +64,6 @@ static int launch_scan_l2_any(ScanParams<typename WideAcc<typename LDR::V, Op>::
   constexpr int IT = ScanItems<T, Op>::value;
   const int subs = l2_subs(p.n);
   p.pre = g_scan_l2_pre;
-  if constexpr (std::is_same<LDR, PlainLoad<float>>::value && std::is_same<Op, OpAdd>::value) {
-    // tile-shape experiments (drk_tune "scan_exp"): sub-tile runs / sub-tiles per tile
-    switch (g_scan_exp) {
-      case 1: return launch_l2_fn((const void*)scan_l2_kernel<LDR, Op, BLOCK, 12, 8, 3>, p, (int64_t)BLOCK * 12 * 8,
-                                  3 * BLOCK * 12 * 4, device, s);
-      case 2: return launch_l2_fn((const void*)scan_l2_kernel<LDR, Op, BLOCK, 20, 2, 3>, p, (int64_t)BLOCK * 20 * 2,
-                                  3 * BLOCK * 20 * 4, device, s);
-      case 3: return launch_l2_fn((const void*)scan_l2_kernel<LDR, Op, BLOCK, 12, 4, 3>, p, (int64_t)BLOCK * 12 * 4,
-                                  3 * BLOCK * 12 * 4, device, s);
-      case 4: return launch_l2_fn((const void*)scan_l2_kernel<LDR, Op, BLOCK, 12, 12, 3>, p, (int64_t)BLOCK * 12 * 12,
-                                  3 * BLOCK * 12 * 4, device, s);
-      default: break;
-    }
-  }
   const int smem = 3 * BLOCK * IT * (int)sizeof(T);
   const void* fn = subs == 4 ? (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 4, 3>
                              : (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 8, 3>;
