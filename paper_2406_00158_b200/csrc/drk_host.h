@@ -40,11 +40,10 @@ extern int g_scan_l2_subs;  // sub-tiles per L2 tile (0: 8 = 160 KB for 4-byte t
 extern int g_scan_l2_pre;   // sub-tiles scanned prefix-free during the look-back
 extern int g_scan_l2_ring;  // TMA ring slots of the L2 re-scan (2 or 3)
 extern int g_scan_debug;    // ScanParams::debug (experiments only)
-extern int g_scan_stagger;
+extern int g_scan_stagger;     // ns between first-wave tile starts of the L2 scan (-1: automatic)
 extern int g_scan_smem_pad;    // extra dynamic smem of the L2 scan (caps CTAs per SM): experiments
-extern int g_scan_rescan_pol;
+extern int g_scan_rescan_pol;  // ScanParams::rescan_pol (experiments)
 extern int g_scan_keep_tail;   // ScanParams::keep_tail
-extern int g_scan_exp;         // tile-shape experiments of the fp32 L2 scan  // ScanParams::rescan_pol  // ns between first-wave tile starts of the L2 scan (-1: automatic)
 extern thread_local int g_chain_launch;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
 extern void* g_scan_trace;  // debug: per-tile timestamps of the next scans
 
