@@ -6,7 +6,9 @@ family once on small and ragged sizes, through the public API, checked against n
 
 Covers map (copy, fill, iota, triad, Black-Scholes, NVRTC maps), reduce (dot, sum/min/max,
 NVRTC reduce), scan (single-pass tiles, the L2 two-touch kernel, chained and batched over
-segments), sort (both strategies: CUB, drk_gather, drk_sort_bounds) and the readback kernel.
+segments), sort (both strategies: the radix sort, drk_gather, drk_sort_bounds) and the readback
+kernel; round 2 adds fused view scans, the keep_tail L2 scan, both Black-Scholes tiers, float64
+radix sorts with NaNs, CUDA-graph replays and the device / NCCL / fused reduce combines.
 """
 import os
 import sys
@@ -68,5 +70,34 @@ for n in sizes:
         s = sr.DistributedVector.from_numpy(rt, xi)
         sr.sort(s, key=lambda v: v % 13, strategy=strategy)
         assert np.array_equal(s.to_numpy(), xi[np.argsort(xi % 13, kind="stable")])
+    # round 2: fused view scans, the keep_tail L2 scan (8 sub-tiles forced), both
+    # Black-Scholes tiers, float64 radix sort with NaNs, graph replays of a cached plan
+    pf = sr.DistributedVector(rt, n, dtype=np.float32)
+    A.inclusive_scan(views.transform(views.zip(vx, vy), lambda t: t[0] * t[1]), pf)
+    A.inclusive_scan(views.transform(vx, lambda v: 2.5 * v + 1.0), pf)
+    _lib.load().drk_tune(b"scan_l2_subs", 8)
+    o = sr.DistributedVector(rt, n, dtype=np.int32)
+    A.inclusive_scan(vi, o)
+    assert np.array_equal(o.to_numpy(), np.cumsum(xi.astype(np.int64)).astype(np.int32))
+    _lib.load().drk_tune(b"scan_l2_subs", 0)
+    for precision in ("reference", "fast"):
+        B.black_scholes_prices(a, *[sr.DistributedVector.from_numpy(rt, (90 + 20 * rng.random(n)).astype(np.float32))
+                                    for _ in range(2)],
+                               *[sr.DistributedVector.from_numpy(rt, (0.1 + 0.2 * rng.random(n)).astype(np.float32))
+                                 for _ in range(3)], precision=precision)
+    xd = rng.standard_normal(n)
+    xd[::5] = np.nan
+    s = sr.DistributedVector.from_numpy(rt, xd)
+    sr.sort(s)
+    assert np.array_equal(s.to_numpy(), np.sort(xd), equal_nan=True)
+    for _ in range(3):  # a cached 3-segment plan: direct launches, then a CUDA graph replay
+        A.for_each(a, lambda v: v * 0.5)
     print(f"n={n} ok", flush=True)
+# round 2: the cross-GPU reduce combines (one GPU: 3 locales, a one-rank communicator)
+for mode in ("device", "nccl", "fused"):
+    with sr.Runtime(3, devices=[0], reduce_combine=mode) as rt2:
+        x = rng.integers(-1000, 1000, 100_003).astype(np.int32)
+        v = sr.DistributedVector.from_numpy(rt2, x)
+        assert A.reduce(v, 0) == int(x.astype(np.int64).sum())
+        assert A.reduce(v, 10**9, A.minimum) == int(x.min())
 print("sanitize workload done")
