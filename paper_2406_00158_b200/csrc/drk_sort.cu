@@ -63,7 +63,10 @@ namespace {
 
 constexpr int RX_BLOCK = 256;
 constexpr int RX_WARPS = RX_BLOCK / 32;
-constexpr int RX_IPT = 16;                       // keys per thread
+#ifndef DRK_RX_IPT
+#define DRK_RX_IPT 16
+#endif
+constexpr int RX_IPT = DRK_RX_IPT;               // keys per thread
 constexpr int RX_TILE = RX_BLOCK * RX_IPT;       // 4096 keys per tile
 constexpr int RX_DIGITS = 256;
 
