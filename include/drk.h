@@ -224,6 +224,28 @@ int drk_reduce_fused(int kind, int dtype, int op, int ndev, const int* devices, 
                      const int* slot_of, void* home_slots, void* home_counter, const void* init,
                      void* result_host_mapped, void* flag_host_mapped, uint64_t epoch, void* const* scratch);
 
+/* One process per GPU: an all-gather of one (has, value) pair per rank over peer memory,
+ * without NCCL.  drk_ipc_alloc allocates (and zeroes) a whole device allocation — a rank's
+ * mailbox of 2 x world x 32 bytes (two banks, alternating by epoch) — drk_ipc_handle exports
+ * it (64-byte cudaIpcMemHandle_t),
+ * drk_ipc_open maps another process's on `device` (peer access enabled lazily), drk_ipc_close /
+ * drk_ipc_free release them.  drk_mailbox_allgather enqueues one kernel: it stores the rank's
+ * 16-byte pair (device memory) into slot `rank` of every mailbox (peer_boxes[j] = rank j's,
+ * mapped; the rank's own included), fences system-wide, stamps the slot with epoch, waits
+ * until every slot of its own mailbox carries epoch and writes the pairs, rank by rank, into
+ * gathered (world x 16 bytes, the layout of an NCCL all-gather).  *status (int, device memory)
+ * becomes 0, or 1 when a rank did not arrive within timeout_ns (gathered is then zero there).
+ * Epochs must increase from call to call and agree across ranks.  world <= DRK_COMM_MAX_RANKS. */
+#define DRK_COMM_MAX_RANKS 32
+int drk_ipc_alloc(size_t bytes, int device, void** dev_ptr);
+int drk_ipc_free(void* dev_ptr);
+int drk_ipc_handle(void* dev_ptr, void* handle_out);
+int drk_ipc_open(const void* handle, int device, void** dev_ptr);
+int drk_ipc_close(void* dev_ptr);
+int drk_mailbox_allgather(const void* pair, void* const* peer_boxes, int world, int rank, const void* own_box,
+                          uint64_t epoch, uint64_t timeout_ns, void* gathered, void* status, int device,
+                          void* stream);
+
 /* CUDA graphs of fixed launch sequences (a cached plan that issues several kernels on one
  * stream): drk_graph_begin starts a thread-local capture on `stream`, the entries called
  * next are captured instead of run, drk_graph_end instantiates them into *exec (the capture

@@ -88,6 +88,12 @@ SIGNATURES = {
     "drk_reduce_fused": (_int, [_int, _int, _int, _int, ctypes.POINTER(_int), ctypes.POINTER(_vp), ctypes.POINTER(_int),
                                 ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_i64), ctypes.POINTER(_int),
                                 _vp, _vp, _vp, _vp, _vp, _u64, ctypes.POINTER(_vp)]),
+    "drk_ipc_alloc": (_int, [_sz, _int, ctypes.POINTER(_vp)]),
+    "drk_ipc_free": (_int, [_vp]),
+    "drk_ipc_handle": (_int, [_vp, _vp]),
+    "drk_ipc_open": (_int, [_vp, _int, ctypes.POINTER(_vp)]),
+    "drk_ipc_close": (_int, [_vp]),
+    "drk_mailbox_allgather": (_int, [_vp, ctypes.POINTER(_vp), _int, _int, _vp, _u64, _u64, _vp, _vp, _int, _vp]),
     "drk_graph_begin": (_int, [_int, _vp]),
     "drk_graph_end": (_int, [_int, _vp, ctypes.POINTER(_vp)]),
     "drk_graph_launch": (_int, [_vp, _int, _vp]),
@@ -225,6 +231,7 @@ SCAN_SEGS = 16  # drk.h DRK_SCAN_SEGS
 RED_SEGS = 16  # drk.h DRK_RED_SEGS
 FOLD_MAX = 64  # drk.h DRK_FOLD_MAX: partials one drk_reduce_fold folds
 COMM_MAX_DEV = 16  # drk.h DRK_COMM_MAX_DEV
+COMM_MAX_RANKS = 32  # drk.h DRK_COMM_MAX_RANKS
 VIEW_PRODUCT, VIEW_AFFINE = 1, 2  # drk.h DRK_VIEW_*
 BS_FAST = 1  # drk.h DRK_BS_FAST
 JIT_WORDS = 16  # drk_device.cuh DRK_JIT_WORDS: 8-byte words of a fused scan loader

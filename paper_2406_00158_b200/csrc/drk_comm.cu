@@ -250,3 +250,114 @@ extern "C" int drk_comm_reduce(void* comm, int dtype, int op, const void* const*
   }
   return 0;
 }
+
+// ---- one process per GPU: an all-gather of (has, value) pairs over peer memory ------------
+// Each rank owns a mailbox (2 banks x world slots of 32 bytes: has, value, epoch, pad) in its GPU's
+// memory, allocated here and exported with a CUDA IPC handle; every rank maps every other
+// rank's mailbox (NVLink peer memory; cudaIpcMemLazyEnablePeerAccess).  One exchange is one
+// kernel per rank: it stores the rank's pair into slot `rank` of every mailbox (peer stores,
+// then a system-scope fence, then the slot's epoch word), waits until every slot of its own
+// mailbox carries this epoch, and copies the pairs into `gathered` (16 bytes per rank, the
+// layout an NCCL all-gather of the pairs produces).  The reduce's and the scan's cross-rank
+// combine then need no NCCL call and no host.  A rank that never arrives does not hang the
+// GPU: the wait gives up after timeout_ns and writes 1 into *status (0 on success).
+
+extern "C" int drk_ipc_alloc(size_t bytes, int device, void** dev_ptr) {
+  if (!dev_ptr || !bytes) return set_error(DRK_E_ARG, "drk_ipc_alloc: bad argument");
+  *dev_ptr = nullptr;
+  if (int rc = prologue(device, "drk_ipc_alloc")) return rc;
+  DRK_CHECK(cudaMalloc(dev_ptr, bytes));  // a whole allocation: its IPC handle maps its base
+  DRK_CHECK(cudaMemset(*dev_ptr, 0, bytes));
+  return 0;
+}
+
+extern "C" int drk_ipc_free(void* dev_ptr) {
+  if (dev_ptr) DRK_CHECK(cudaFree(dev_ptr));
+  return 0;
+}
+
+extern "C" int drk_ipc_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return set_error(DRK_E_ARG, "drk_ipc_handle: null argument");
+  cudaIpcMemHandle_t h;
+  DRK_CHECK(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle_out, &h, sizeof(h));
+  return 0;
+}
+
+extern "C" int drk_ipc_open(const void* handle, int device, void** dev_ptr) {
+  if (!handle || !dev_ptr) return set_error(DRK_E_ARG, "drk_ipc_open: null argument");
+  *dev_ptr = nullptr;
+  if (int rc = prologue(device, "drk_ipc_open")) return rc;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  DRK_CHECK(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return 0;
+}
+
+extern "C" int drk_ipc_close(void* dev_ptr) {
+  if (dev_ptr) DRK_CHECK(cudaIpcCloseMemHandle(dev_ptr));
+  return 0;
+}
+
+namespace {
+struct Mailboxes {
+  unsigned long long* box[DRK_COMM_MAX_RANKS];
+};
+
+__global__ void mailbox_allgather_kernel(const unsigned long long* __restrict__ pair, const Mailboxes mb, int world,
+                                         int rank, const volatile unsigned long long* own, unsigned long long epoch,
+                                         unsigned long long timeout_ns, unsigned long long* gathered, int* status) {
+  // two banks alternate by epoch: a rank that finished exchange e may already publish e + 1
+  // before a slower rank has read exchange e, but not e + 2 (that needs the slower rank's e + 1)
+  const int bank = (int)(epoch & 1ull) * world;
+  const int j = threadIdx.x;
+  if (j < world) {  // publish: the pair, then (after a system fence) this exchange's epoch
+    unsigned long long* slot = mb.box[j] + 4 * (bank + rank);
+    slot[0] = pair[0];
+    slot[1] = pair[1];
+    __threadfence_system();
+    *(volatile unsigned long long*)(slot + 2) = epoch;
+  }
+  __syncwarp();
+  int ok = 1;
+  if (j < world) {
+    unsigned long long t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const volatile unsigned long long* mine = own + 4 * (bank + j);
+    while (mine[2] != epoch) {
+      __nanosleep(128);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > timeout_ns) {
+        ok = 0;
+        break;
+      }
+    }
+    __threadfence_system();
+    gathered[2 * j] = ok ? mine[0] : 0ull;
+    gathered[2 * j + 1] = ok ? mine[1] : 0ull;
+  }
+  const int all = __all_sync(0xffffffffu, ok);
+  if (j == 0) *status = all ? 0 : 1;
+}
+}  // namespace
+
+extern "C" int drk_mailbox_allgather(const void* pair, void* const* peer_boxes, int world, int rank, const void* own_box,
+                                     uint64_t epoch, uint64_t timeout_ns, void* gathered, void* status, int device,
+                                     void* stream) {
+  if (!pair || !peer_boxes || !own_box || !gathered || !status)
+    return set_error(DRK_E_ARG, "drk_mailbox_allgather: null argument");
+  if (world < 1 || world > DRK_COMM_MAX_RANKS || rank < 0 || rank >= world)
+    return set_error(DRK_E_ARG, "drk_mailbox_allgather: rank / world out of range");
+  Mailboxes mb;
+  memset(&mb, 0, sizeof(mb));
+  for (int j = 0; j < world; ++j) {
+    if (!peer_boxes[j]) return set_error(DRK_E_ARG, "drk_mailbox_allgather: null mailbox");
+    mb.box[j] = (unsigned long long*)peer_boxes[j];
+  }
+  if (int rc = prologue(device, "drk_mailbox_allgather")) return rc;
+  mailbox_allgather_kernel<<<1, 32, 0, (cudaStream_t)stream>>>((const unsigned long long*)pair, mb, world, rank,
+                                                               (const volatile unsigned long long*)own_box, epoch,
+                                                               timeout_ns, (unsigned long long*)gathered, (int*)status);
+  drk_note_launch();
+  return epilogue("drk_mailbox_allgather");
+}

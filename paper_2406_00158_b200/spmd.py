@@ -21,6 +21,7 @@ tested on hosts without GPUs.
 from __future__ import annotations
 
 import operator
+import os
 
 import numpy as np
 
@@ -44,7 +45,7 @@ def _dist():
 class Group:
     """A torch.distributed process group (default: the world)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, combine=None):
         dist = _dist()
         if not dist.is_initialized():
             raise RuntimeError("torch.distributed is not initialised (launch with torchrun)")
@@ -52,12 +53,76 @@ class Group:
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
         self.backend = dist.get_backend(group)
+        # how the reduce / scan exchange of (has, value) pairs runs: "collective" — an
+        # all-gather of the backend (NCCL on the rank's stream); "ipc" — the library's own
+        # kernel over peer memory (every rank's mailbox mapped with CUDA IPC, no NCCL call)
+        combine = combine or os.environ.get("DRK_SPMD_COMBINE", "collective")
+        if combine not in ("collective", "ipc"):
+            raise ValueError(f"unknown combine {combine!r} (collective or ipc)")
+        if combine == "ipc" and self.size > _lib.COMM_MAX_RANKS:
+            raise ValueError(f"combine='ipc' supports up to {_lib.COMM_MAX_RANKS} ranks")
+        self.combine = combine
+        self._mailbox = None
+
+    def mailbox(self, state):
+        """The rank's peer-memory mailbox (created collectively on first use)."""
+        if self._mailbox is None:
+            self._mailbox = _Mailbox(self, state)
+        return self._mailbox
 
     def device(self):
         t = _torch()
         if self.backend == "nccl":
             return t.device("cuda", t.cuda.current_device())
         return t.device("cpu")
+
+
+class _Mailbox:
+    """Every rank's mailbox mapped into this rank (drk_ipc_*), for drk_mailbox_allgather: the
+    all-gather of one (has, value) pair per rank as one kernel over NVLink peer memory."""
+
+    TIMEOUT_NS = 120 * 10**9  # a rank that never arrives: an error after two minutes, not a hang
+
+    def __init__(self, group: Group, state):
+        import ctypes
+
+        dist = _dist()
+        self.group, self.state = group, state
+        own = ctypes.c_void_p()
+        _lib.call("drk_ipc_alloc", 2 * group.size * 32, state.index, ctypes.byref(own))
+        self.own = own.value
+        handle = ctypes.create_string_buffer(64)
+        _lib.call("drk_ipc_handle", self.own, handle)
+        handles = [None] * group.size
+        dist.all_gather_object(handles, handle.raw, group=group.group)
+        peers, self.opened = [], []
+        for j, h in enumerate(handles):
+            if j == group.rank:
+                peers.append(self.own)
+                continue
+            p = ctypes.c_void_p()
+            _lib.call("drk_ipc_open", ctypes.create_string_buffer(h, 64), state.index, ctypes.byref(p))
+            peers.append(p.value)
+            self.opened.append(p.value)
+        self.peers = (ctypes.c_void_p * group.size)(*peers)
+        self.epoch = 0
+        dist.barrier(group=group.group)  # every mailbox mapped before anyone writes
+
+    def allgather(self, pair, gathered, status):
+        """Enqueue the exchange on the rank's stream (pair: 16 device bytes; gathered: world x
+        16 device bytes; status: a device int32 that becomes 1 if a rank did not arrive)."""
+        self.epoch += 1
+        st, g = self.state, self.group
+        _lib.call("drk_mailbox_allgather", pair.data_ptr(), self.peers, g.size, g.rank, self.own, self.epoch,
+                  self.TIMEOUT_NS, gathered.data_ptr(), status.data_ptr(), st.index, st.handle)
+
+    def __del__(self):
+        try:
+            for p in self.opened:
+                _lib.call("drk_ipc_close", p)
+            _lib.call("drk_ipc_free", self.own)
+        except Exception:  # pragma: no cover - interpreter teardown
+            pass
 
 
 _REDUCE_OPS = {"add": "SUM", "multiply": "PRODUCT", "minimum": "MIN", "maximum": "MAX"}
@@ -106,19 +171,28 @@ def gather_pairs(value, acc_dtype, group: Group, state=None) -> list:
     pair = np.zeros(2, dtype=np.int64)
     if value is not None:
         pair[0], pair[1] = 1 + _PAIR_DTYPES.index(A), _encode(value, A)
-    if group.backend == "nccl" and state is not None:
+    ipc = group.combine == "ipc" and state is not None
+    if (group.backend == "nccl" or ipc) and state is not None:
         with t.cuda.stream(state.stream):
             buf = t.empty(2, dtype=t.int64, device=state.device)
-            out = t.empty(2 * group.size, dtype=t.int64, device=state.device)
+            out = t.empty(2 * group.size + 1, dtype=t.int64, device=state.device)
         for k in range(2):
             w = np.array([pair[k]], dtype=np.int64)
             _lib.call("drk_fill", _lib.I64, buf.data_ptr() + 8 * k, 1, w.ctypes.data, state.index, state.handle)
-        with t.cuda.device(state.index), t.cuda.stream(state.stream):
-            dist.all_gather_into_tensor(out, buf, group=group.group)
-        host = t.empty(2 * group.size, dtype=t.int64, pin_memory=True)
-        _lib.call("drk_readback", host.data_ptr(), out.data_ptr(), 16 * group.size, state.index, state.handle)
+        if ipc:
+            status = out[2 * group.size:]
+            _lib.call("drk_memset_async", status.data_ptr(), 0, 8, state.index, state.handle)
+            group.mailbox(state).allgather(buf, out, status)
+        else:
+            with t.cuda.device(state.index), t.cuda.stream(state.stream):
+                dist.all_gather_into_tensor(out[: 2 * group.size], buf, group=group.group)
+        host = t.empty(2 * group.size + 1, dtype=t.int64, pin_memory=True)
+        _lib.call("drk_readback", host.data_ptr(), out.data_ptr(), 8 * (2 * group.size + 1), state.index,
+                  state.handle)
         state.synchronize()
-        got = host.numpy().reshape(group.size, 2)
+        if ipc and host.numpy()[2 * group.size] & 0xFFFFFFFF:
+            raise RuntimeError("spmd: a rank did not reach the peer-memory exchange in time")
+        got = host.numpy()[: 2 * group.size].reshape(group.size, 2)
     else:
         x = t.from_numpy(pair).to(group.device())
         outs = t.empty(2 * group.size, dtype=t.int64, device=x.device)
@@ -240,7 +314,8 @@ def _scan(local, out, group, op, exclusive, init):
     acc = _lib.acc_dtype(T, opcode)
     pieces = A._pieces(local)
     st = _state_of(A.runtime_of(local), local) if pieces else None
-    if pieces and st is not None and group.backend == "nccl" and group.size <= _lib.CARRY_MAX:
+    if pieces and st is not None and (group.backend == "nccl" or group.combine == "ipc") \
+            and group.size <= _lib.CARRY_MAX:
         # device path: local totals -> (has, total) pair -> all-gather -> carry, all on the
         # rank's stream; the host only checks the int32 carry range after the scan
         return A._scan_impl(local, out, op, exclusive, init,
@@ -266,17 +341,22 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
     A = np.dtype(acc)
 
     def hook(total_ptrs, st):
+        ipc = group.combine == "ipc"
         with t.cuda.stream(st.stream):
             pair = t.zeros(2, dtype=t.int64, device=st.device)
             gathered = t.empty(2 * group.size, dtype=t.int64, device=st.device)
             carry = t.zeros(1, dtype=t.int64, device=st.device)
+            status = t.zeros(1, dtype=t.int64, device=st.device)
         one = np.array([1], dtype=np.int64)
         _lib.call("drk_fill", _lib.I64, pair.data_ptr(), 1, one.ctypes.data, st.index, st.handle)
         vals = (ctypes.c_void_p * len(total_ptrs))(*total_ptrs)
         _lib.call("drk_carry_fold", code, opcode, vals, None, len(total_ptrs), None, None, pair.data_ptr() + 8,
                   st.index, st.handle)
-        with t.cuda.device(st.index), t.cuda.stream(st.stream):
-            dist.all_gather_into_tensor(gathered, pair, group=group.group)
+        if ipc:
+            group.mailbox(st).allgather(pair, gathered, status)
+        else:
+            with t.cuda.device(st.index), t.cuda.stream(st.stream):
+                dist.all_gather_into_tensor(gathered, pair, group=group.group)
         r = group.rank
         carry_ptr = None
         if r > 0:
@@ -292,6 +372,8 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
             host = t.empty(2 * group.size, dtype=t.int64, pin_memory=True)
             _lib.call("drk_readback", host.data_ptr(), gathered.data_ptr(), 16 * group.size, st.index, st.handle)
             st.synchronize()
+            if ipc and int(status.cpu()[0]) & 0xFFFFFFFF:
+                raise RuntimeError("spmd: a rank did not reach the peer-memory exchange in time")
             raw = host.numpy().tobytes()
             fold = _PYOPS[opname]
             c = None
@@ -299,7 +381,7 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
                 if np.frombuffer(raw[16 * j: 16 * j + 8], dtype=np.int64)[0]:
                     v = np.frombuffer(raw[16 * j + 8: 16 * j + 8 + A.itemsize], dtype=A)[0]
                     c = v if c is None else fold(c, v)
-            _keep = (pair, gathered, carry)  # noqa: F841 - alive until the scan has run
+            _keep = (pair, gathered, carry, status)  # noqa: F841 - alive until the scan has run
             return c
 
         return carry_ptr, host_value
