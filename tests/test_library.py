@@ -95,3 +95,17 @@ def test_round2_entries_validate_before_any_launch():
     assert lib.drk_partial_dtype(_lib.F32, _lib.ADD) == _lib.F32
     assert lib.drk_partial_dtype(_lib.I32, _lib.ADD) == _lib.I64
     assert lib.drk_partial_dtype(_lib.I32, _lib.MIN) == _lib.I32
+
+
+def test_ipc_entries_validate_before_any_launch():
+    lib = _lib.load()
+    vp = ctypes.c_void_p
+    p = vp()
+    assert lib.drk_ipc_alloc(0, 0, ctypes.byref(p)) == _lib.E_ARG
+    assert lib.drk_ipc_handle(None, None) == _lib.E_ARG
+    assert lib.drk_ipc_open(None, 0, ctypes.byref(p)) == _lib.E_ARG
+    assert lib.drk_ipc_close(None) == 0 and lib.drk_ipc_free(None) == 0
+    assert lib.drk_mailbox_allgather(None, None, 2, 0, None, 1, 1, None, None, 0, None) == _lib.E_ARG
+    boxes = (vp * 2)(1, 1)
+    assert lib.drk_mailbox_allgather(1, boxes, 2, 2, 1, 1, 1, 1, 1, 0, None) == _lib.E_ARG
+    assert "range" in _lib.last_error()
