@@ -871,7 +871,7 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
 
     if carry_hook is not None or (len(work) <= _lib.CARRY_MAX + 1 and not _FORCE_HOST_CARRY):
         return _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, init, init_a, carry,
-                                  launches, carry_hook)
+                                  launches, carry_hook, want_partials)
     # several devices, host carry (more segments than drk_carry_fold takes): totals first
     # (all GPUs in parallel), carries on the host exactly as the reference's driver loop,
     # then one carried scan per segment.
@@ -950,7 +950,7 @@ def _scan_batched(work, partials, live, st, op, opcode, T, A, L, exclusive, init
 
 
 def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, init, init_a, carry, launches,
-                       carry_hook=None):
+                       carry_hook=None, want_partials=True):
     """Scan of segments spread over several GPUs with the carry folded on the devices.
 
     1. Every segment's total is reduced on its own GPU (all GPUs in parallel).
@@ -1012,6 +1012,8 @@ def _scan_device_carry(work, partials, live, op, opcode, T, A, L, exclusive, ini
             kernels.launch_kernel("drk_carry_fold", launch, 1, code, opcode, vals, None, len(before),
                                   ctypes.addressof(carry_buf) if carry_buf is not None else None, in_dev, carry_dev)
         _run_segment_scan(T, opcode, exclusive, in_ptr, tgt, launch, init=init_a, carry_dev=carry_dev)
+    if not want_partials and not _needs_range_check(T):
+        return partials  # nothing to read back: the scans stay asynchronous on their streams
     raw = {}
     for k, st, *_ in work:
         if id(st) not in raw:

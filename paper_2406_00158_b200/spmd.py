@@ -56,13 +56,57 @@ class Group:
         # how the reduce / scan exchange of (has, value) pairs runs: "collective" — an
         # all-gather of the backend (NCCL on the rank's stream); "ipc" — the library's own
         # kernel over peer memory (every rank's mailbox mapped with CUDA IPC, no NCCL call)
-        combine = combine or os.environ.get("DRK_SPMD_COMBINE", "collective")
-        if combine not in ("collective", "ipc"):
-            raise ValueError(f"unknown combine {combine!r} (collective or ipc)")
+        # "auto" (the default) uses "ipc" when every rank can map every other rank's mailbox
+        # and a trial exchange returns every rank's pair, else "collective" — decided
+        # collectively on first use (_decide)
+        combine = combine or os.environ.get("DRK_SPMD_COMBINE", "auto")
+        if combine not in ("collective", "ipc", "auto"):
+            raise ValueError(f"unknown combine {combine!r} (collective, ipc or auto)")
         if combine == "ipc" and self.size > _lib.COMM_MAX_RANKS:
             raise ValueError(f"combine='ipc' supports up to {_lib.COMM_MAX_RANKS} ranks")
-        self.combine = combine
+        if combine == "auto" and self.size > _lib.COMM_MAX_RANKS:
+            combine = "collective"
+        self._combine = combine
         self._mailbox = None
+
+    @property
+    def combine(self):
+        return self._combine
+
+    def decide(self, state):
+        """Resolve combine="auto" (collective: every rank must call it at the same point)."""
+        if self._combine != "auto":
+            return self._combine
+        dist = _dist()
+        mb, ok = None, True
+        try:
+            mb = _Mailbox(self, state)
+            ok = mb.trial()
+        except Exception:  # no IPC / peer access between these GPUs: the backend's collective
+            ok = False
+        flags = [None] * self.size
+        dist.all_gather_object(flags, ok, group=self.group)
+        if all(flags):
+            self._mailbox, self._combine = mb, "ipc"
+        else:
+            self._combine = "collective"
+            del mb
+        return self._combine
+
+    def exchange_buffers(self, state):
+        """Persistent buffers of gather_pairs on the rank's GPU (reused call after call: every
+        exchange is complete, and read back, before the next one starts)."""
+        bufs = getattr(self, "_xbufs", None)
+        if bufs is None:
+            bufs = self._xbufs = _ExchangeBuffers(self, state)
+        return bufs
+
+    def scan_buffers(self, state):
+        """Persistent device buffers of the scan's carry exchange on the rank's GPU."""
+        b = getattr(self, "_sbufs", None)
+        if b is None:
+            b = self._sbufs = _ScanBuffers(self, state)
+        return b
 
     def mailbox(self, state):
         """The rank's peer-memory mailbox (created collectively on first use)."""
@@ -75,6 +119,56 @@ class Group:
         if self.backend == "nccl":
             return t.device("cuda", t.cuda.current_device())
         return t.device("cpu")
+
+
+class _ExchangeBuffers:
+    """The (has, value) pair in mapped pinned memory (host-written, kernel-read), its device
+    copy for NCCL, the gathered pairs + a status word on the device, and their host copy."""
+
+    def __init__(self, group: Group, state):
+        import ctypes
+
+        t = _torch()
+        n = 2 * group.size + 1
+        self.pair_host = t.zeros(2, dtype=t.int64, pin_memory=True)
+        self.pair_np = self.pair_host.numpy()
+        self.pair_host_ptr = self.pair_host.data_ptr()
+        dev = ctypes.c_void_p()
+        _lib.call("drk_mapped_ptr", self.pair_host_ptr, ctypes.byref(dev))
+        self.pair_dev = _Ptr(int(dev.value))
+        with t.cuda.stream(state.stream):
+            self.buf = t.zeros(2, dtype=t.int64, device=state.device)
+            self.out = t.zeros(n, dtype=t.int64, device=state.device)
+        self.status = self.out[2 * group.size:]
+        self.status_ptr = self.status.data_ptr()
+        self.host = t.zeros(n, dtype=t.int64, pin_memory=True)
+        self.host_np = self.host.numpy()
+
+
+class _ScanBuffers:
+    """pair (has, total), gathered pairs followed by the exchange status word, and the carry."""
+
+    def __init__(self, group: Group, state):
+        t = _torch()
+        with t.cuda.stream(state.stream):
+            self.pair = t.zeros(2, dtype=t.int64, device=state.device)
+            g = t.zeros(2 * group.size + 1, dtype=t.int64, device=state.device)
+            self.carry = t.zeros(1, dtype=t.int64, device=state.device)
+        self.gathered = g
+        self.status = g[2 * group.size:]
+        self.one = np.array([1], dtype=np.int64)
+
+
+class _Ptr:
+    """A raw device address with the data_ptr() of a tensor."""
+
+    __slots__ = ("p",)
+
+    def __init__(self, p):
+        self.p = p
+
+    def data_ptr(self):
+        return self.p
 
 
 class _Mailbox:
@@ -107,6 +201,21 @@ class _Mailbox:
         self.peers = (ctypes.c_void_p * group.size)(*peers)
         self.epoch = 0
         dist.barrier(group=group.group)  # every mailbox mapped before anyone writes
+
+    def trial(self, timeout_ns=10 * 10**9) -> bool:
+        """One exchange of (1, rank): True when every rank's pair arrived in place."""
+        t = _torch()
+        st, g = self.state, self.group
+        with t.cuda.stream(st.stream):
+            pair = t.tensor([1, g.rank], dtype=t.int64).to(st.device)
+            out = t.zeros(2 * g.size + 1, dtype=t.int64, device=st.device)
+        self.epoch += 1
+        _lib.call("drk_mailbox_allgather", pair.data_ptr(), self.peers, g.size, g.rank, self.own, self.epoch,
+                  timeout_ns, out.data_ptr(), out.data_ptr() + 16 * g.size, st.index, st.handle)
+        st.synchronize()
+        got = out.cpu().numpy()
+        want = np.array([[1, j] for j in range(g.size)], dtype=np.int64).ravel()
+        return bool(np.array_equal(got[: 2 * g.size], want) and (got[2 * g.size] & 0xFFFFFFFF) == 0)
 
     def allgather(self, pair, gathered, status):
         """Enqueue the exchange on the rank's stream (pair: 16 device bytes; gathered: world x
@@ -171,28 +280,29 @@ def gather_pairs(value, acc_dtype, group: Group, state=None) -> list:
     pair = np.zeros(2, dtype=np.int64)
     if value is not None:
         pair[0], pair[1] = 1 + _PAIR_DTYPES.index(A), _encode(value, A)
-    ipc = group.combine == "ipc" and state is not None
+    ipc = state is not None and group.decide(state) == "ipc"
     if (group.backend == "nccl" or ipc) and state is not None:
-        with t.cuda.stream(state.stream):
-            buf = t.empty(2, dtype=t.int64, device=state.device)
-            out = t.empty(2 * group.size + 1, dtype=t.int64, device=state.device)
-        for k in range(2):
-            w = np.array([pair[k]], dtype=np.int64)
-            _lib.call("drk_fill", _lib.I64, buf.data_ptr() + 8 * k, 1, w.ctypes.data, state.index, state.handle)
+        x = group.exchange_buffers(state)
         if ipc:
-            status = out[2 * group.size:]
-            _lib.call("drk_memset_async", status.data_ptr(), 0, 8, state.index, state.handle)
-            group.mailbox(state).allgather(buf, out, status)
+            # the pair goes straight from the host into mapped memory, which the exchange
+            # kernel reads as device memory: one kernel, one readback, one wait
+            x.pair_np[:] = pair
+            _lib.call("drk_memset_async", x.status_ptr, 0, 8, state.index, state.handle)
+            group.mailbox(state).allgather(x.pair_dev, x.out, x.status)
         else:
+            x.pair_np[:] = pair
+            # a kernel copy from mapped memory (a copy-engine transfer could queue behind bulk
+            # PCIe traffic on another stream)
+            _lib.call("drk_copy", _lib.I64, x.buf.data_ptr(), x.pair_dev.p, 2, state.index, state.handle)
             with t.cuda.device(state.index), t.cuda.stream(state.stream):
-                dist.all_gather_into_tensor(out[: 2 * group.size], buf, group=group.group)
-        host = t.empty(2 * group.size + 1, dtype=t.int64, pin_memory=True)
-        _lib.call("drk_readback", host.data_ptr(), out.data_ptr(), 8 * (2 * group.size + 1), state.index,
+                dist.all_gather_into_tensor(x.out[: 2 * group.size], x.buf, group=group.group)
+        _lib.call("drk_readback", x.host.data_ptr(), x.out.data_ptr(), 8 * (2 * group.size + 1), state.index,
                   state.handle)
         state.synchronize()
-        if ipc and host.numpy()[2 * group.size] & 0xFFFFFFFF:
+        h = x.host_np
+        if ipc and h[2 * group.size] & 0xFFFFFFFF:
             raise RuntimeError("spmd: a rank did not reach the peer-memory exchange in time")
-        got = host.numpy()[: 2 * group.size].reshape(group.size, 2)
+        got = h[: 2 * group.size].reshape(group.size, 2)
     else:
         x = t.from_numpy(pair).to(group.device())
         outs = t.empty(2 * group.size, dtype=t.int64, device=x.device)
@@ -245,12 +355,18 @@ def reduce(local, init, op, group: Group):
     opname = getattr(op.ufunc, "__name__", None)
     if opname not in _REDUCE_OPS:
         raise TypeError("distributed reduce needs add/multiply/minimum/maximum")
-    pieces = A._pieces(local)
+    from . import plans
+
     rt = A.runtime_of(local)
+    opk = A._op_key(op)
+    key, dvs, plan = plans.lookup("spmd_reduce", local, opk) if opk is not None else (None, None, None)
+    if plan is None:  # the rank's lowered pieces, memoised like algorithms.reduce (False: none)
+        pieces = A._pieces(local)
+        plan = plans.store(key, dvs, A._ReducePlan(rt, pieces, op) if pieces else False)
     partial = None
     vdt = None
-    if pieces:
-        parts = A._segment_partials(rt, pieces, op)
+    if plan:
+        parts = plan.run()
         vdt = np.asarray(parts[0]).dtype
         for p in parts:
             partial = p if partial is None else op.fn(partial, p)
@@ -313,20 +429,22 @@ def _scan(local, out, group, op, exclusive, init):
     opcode = A.OPCODES[opname]
     acc = _lib.acc_dtype(T, opcode)
     pieces = A._pieces(local)
-    st = _state_of(A.runtime_of(local), local) if pieces else None
-    if pieces and st is not None and (group.backend == "nccl" or group.combine == "ipc") \
+    st = _state_of(A.runtime_of(local), local)  # every rank, so the collective choices agree
+    if pieces and st is not None and (group.backend == "nccl" or group.decide(st) == "ipc") \
             and group.size <= _lib.CARRY_MAX:
         # device path: local totals -> (has, total) pair -> all-gather -> carry, all on the
         # rank's stream; the host only checks the int32 carry range after the scan
-        return A._scan_impl(local, out, op, exclusive, init,
-                            carry_hook=_device_carry_hook(group, _lib.dtype_code(T), opcode, opname, acc))
+        A._scan_impl(local, out, op, exclusive, init, want_partials=False,
+                     carry_hook=_device_carry_hook(group, _lib.dtype_code(T), opcode, opname, acc))
+        return None
     total = None
     if pieces:
         rt = A.runtime_of(local)
         for p in A._segment_partials(rt, pieces, op):
             total = p if total is None else op.fn(total, p)
     carry = exclusive_carry(None if total is None else acc.type(total), opname, acc, group, st)
-    return A._scan_impl(local, out, op, exclusive, init, carry=carry)
+    A._scan_impl(local, out, op, exclusive, init, carry=carry, want_partials=False)
+    return None
 
 
 def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
@@ -341,14 +459,13 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
     A = np.dtype(acc)
 
     def hook(total_ptrs, st):
-        ipc = group.combine == "ipc"
-        with t.cuda.stream(st.stream):
-            pair = t.zeros(2, dtype=t.int64, device=st.device)
-            gathered = t.empty(2 * group.size, dtype=t.int64, device=st.device)
-            carry = t.zeros(1, dtype=t.int64, device=st.device)
-            status = t.zeros(1, dtype=t.int64, device=st.device)
-        one = np.array([1], dtype=np.int64)
-        _lib.call("drk_fill", _lib.I64, pair.data_ptr(), 1, one.ctypes.data, st.index, st.handle)
+        ipc = group.decide(st) == "ipc"
+        # persistent per (group, GPU): consecutive scans use them in stream order
+        b = group.scan_buffers(st)
+        pair, gathered, carry, status = b.pair, b.gathered, b.carry, b.status
+        _lib.call("drk_fill", _lib.I64, pair.data_ptr(), 1, b.one.ctypes.data, st.index, st.handle)
+        if ipc:
+            _lib.call("drk_memset_async", status.data_ptr(), 0, 8, st.index, st.handle)
         vals = (ctypes.c_void_p * len(total_ptrs))(*total_ptrs)
         _lib.call("drk_carry_fold", code, opcode, vals, None, len(total_ptrs), None, None, pair.data_ptr() + 8,
                   st.index, st.handle)
@@ -356,7 +473,7 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
             group.mailbox(st).allgather(pair, gathered, status)
         else:
             with t.cuda.device(st.index), t.cuda.stream(st.stream):
-                dist.all_gather_into_tensor(gathered, pair, group=group.group)
+                dist.all_gather_into_tensor(gathered[: 2 * group.size], pair, group=group.group)
         r = group.rank
         carry_ptr = None
         if r > 0:
@@ -369,10 +486,11 @@ def _device_carry_hook(group: Group, code: int, opcode: int, opname: str, acc):
 
         def host_value():
             """The carry as the host path computes it (after the scan has completed)."""
-            host = t.empty(2 * group.size, dtype=t.int64, pin_memory=True)
-            _lib.call("drk_readback", host.data_ptr(), gathered.data_ptr(), 16 * group.size, st.index, st.handle)
+            host = t.empty(2 * group.size + 1, dtype=t.int64, pin_memory=True)
+            _lib.call("drk_readback", host.data_ptr(), gathered.data_ptr(), 8 * (2 * group.size + 1), st.index,
+                      st.handle)
             st.synchronize()
-            if ipc and int(status.cpu()[0]) & 0xFFFFFFFF:
+            if ipc and int(host.numpy()[2 * group.size]) & 0xFFFFFFFF:
                 raise RuntimeError("spmd: a rank did not reach the peer-memory exchange in time")
             raw = host.numpy().tobytes()
             fold = _PYOPS[opname]

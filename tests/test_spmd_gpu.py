@@ -33,7 +33,7 @@ def test_spmd_three_ranks_one_gpu():
 def test_spmd_nccl_one_rank():
     # the NCCL exchange itself (fill kernels -> all_gather_into_tensor on the compute stream
     # -> kernel readback) on a world of one: the only NCCL world one GPU can host
-    env = dict(os.environ, SPMD_BACKEND="nccl")
+    env = dict(os.environ, SPMD_BACKEND="nccl", DRK_SPMD_COMBINE="collective")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "spmd_check.py")]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
@@ -54,8 +54,9 @@ def test_bench_two_ranks_shared_gpu(combine):
 
 
 def test_spmd_three_ranks_peer_memory_exchange():
-    # the reduce / scan exchange as the library's own kernel over CUDA-IPC-mapped mailboxes
-    # (DRK_SPMD_COMBINE=ipc), three processes on one GPU; setup over gloo, no NCCL
+    # the reduce / scan exchange forced onto the library's own kernel over CUDA-IPC-mapped
+    # mailboxes (DRK_SPMD_COMBINE=ipc; "auto", the default, picks it after a trial exchange),
+    # three processes on one GPU; setup over gloo, no NCCL
     env = dict(os.environ, DRK_SPMD_COMBINE="ipc")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "3",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tools", "spmd_check.py")]
