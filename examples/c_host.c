@@ -13,6 +13,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 #include <stdlib.h>
 
 #include "../include/drk.h"
@@ -80,6 +81,21 @@ int main(int argc, char** argv) {
   CK(drk_scan(DRK_I32, DRK_ADD, 0, xi, yi, half, NULL, NULL, NULL, NULL, &res[2], scan_scratch, sb, dev, s));
   CK(drk_scan(DRK_I32, DRK_ADD, 0, xi + half, yi + half, n - half, NULL, NULL, &res[2], NULL, NULL, scan_scratch,
               sb, dev, s));
+  /* the driver's fold of the two dot partials on the device (drk_reduce_fold: numpy's
+   * reduce dtype, float32 for float32 data), starting from init 0.0f */
+  const float zero = 0.0f;
+  const void* parts[2] = {&res[0], &res[1]};
+  CK(drk_reduce_fold(DRK_F32, DRK_ADD, parts, 2, &zero, &res[3], NULL, dev, s));
+  /* sort a copy of x with the library's radix sort */
+  int32_t *sx, *salt;
+  CU(cudaMalloc((void**)&sx, n * sizeof(int32_t)));
+  CU(cudaMalloc((void**)&salt, n * sizeof(int32_t)));
+  CU(cudaMemcpyAsync(sx, xi, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  size_t sort_bytes = 0;
+  CK(drk_sort_keys(DRK_I32, sx, salt, n, NULL, &sort_bytes, dev, s));
+  void* sort_scratch = NULL;
+  CU(cudaMalloc(&sort_scratch, sort_bytes));
+  CK(drk_sort_keys(DRK_I32, sx, salt, n, sort_scratch, &sort_bytes, dev, s));
   CK(drk_stream_synchronize(dev, s));
 
   /* host checks */
@@ -94,9 +110,14 @@ int main(int argc, char** argv) {
   CU(cudaMemcpy(ha, a, n * sizeof(float), cudaMemcpyDeviceToHost));
   CU(cudaMemcpy(hx, xi, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
   CU(cudaMemcpy(hy, yi, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(hres, res, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(hres, res, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  int32_t* hs = (int32_t*)malloc(n * sizeof(int32_t));
+  CU(cudaMemcpy(hs, sx, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
   double dot = 0.0, want = 0.0;
   dot = (double)(float)hres[0] + (double)(float)hres[1];
+  float folded;
+  memcpy(&folded, &hres[3], sizeof(float));
+  const int fold_ok = folded == (float)(zero + (float)hres[0]) + (float)hres[1];
   int bad_triad = 0, bad_scan = 0;
   int64_t run = 0;
   for (int64_t i = 0; i < n; ++i) {
@@ -106,10 +127,23 @@ int main(int argc, char** argv) {
     run += hx[i];
     if (hy[i] != (int32_t)run) ++bad_scan;
   }
+  /* sorted, and the same multiset (the sum and the count of each residue mod 7) */
+  int bad_sort = 0;
+  int64_t sum_x = 0, sum_s = 0;
+  int64_t res_x[7] = {0}, res_s[7] = {0};
+  for (int64_t i = 0; i < n; ++i) {
+    if (i && hs[i - 1] > hs[i]) ++bad_sort;
+    sum_x += hx[i];
+    sum_s += hs[i];
+    ++res_x[((hx[i] % 7) + 7) % 7];
+    ++res_s[((hs[i] % 7) + 7) % 7];
+  }
+  if (sum_x != sum_s || memcmp(res_x, res_s, sizeof(res_x))) ++bad_sort;
   const double rel = fabs(dot - want) / fabs(want);
-  const int ok = rel <= 1e-5 && bad_triad == 0 && bad_scan == 0;
+  const int ok = rel <= 1e-5 && bad_triad == 0 && bad_scan == 0 && bad_sort == 0 && fold_ok;
   printf("{\"n\": %lld, \"dot\": %.9g, \"dot_rel_err\": %.3g, \"triad_mismatches\": %d, \"scan_mismatches\": %d, "
-         "\"launches\": %lld, \"ok\": %s}\n",
-         (long long)n, dot, rel, bad_triad, bad_scan, (long long)drk_launch_count(), ok ? "true" : "false");
+         "\"sort_errors\": %d, \"device_fold_ok\": %s, \"launches\": %lld, \"ok\": %s}\n",
+         (long long)n, dot, rel, bad_triad, bad_scan, bad_sort, fold_ok ? "true" : "false",
+         (long long)drk_launch_count(), ok ? "true" : "false");
   return ok ? 0 : 1;
 }

@@ -1,5 +1,6 @@
-"""The C ABI used from plain C (examples/c_host.c): dot, triad and a two-segment scan with
-the carry passed on the device, checked by the C program itself against host loops."""
+"""The C ABI used from plain C (examples/c_host.c): dot, triad, a two-segment scan with the
+carry passed on the device, the device fold of the dot partials and the radix sort, checked
+by the C program itself against host loops."""
 
 import json
 import os
@@ -19,4 +20,5 @@ def test_c_host_program():
     assert out.returncode == 0, out.stdout + out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["ok"] and res["triad_mismatches"] == 0 and res["scan_mismatches"] == 0
+    assert res["sort_errors"] == 0 and res["device_fold_ok"]
     assert res["launches"] >= 8
