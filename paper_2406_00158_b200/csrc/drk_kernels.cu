@@ -384,6 +384,10 @@ template <class T, class M = BSMath<T>> struct BlackScholesF {
 #define BS_REF_E 1
 #endif
   static constexpr int E = (is_same<M, BSMath<T>>::value ? BS_E : BS_REF_E) * 16 / sizeof(T);
+#ifndef BS_REF_MINB
+#define BS_REF_MINB 4
+#endif
+  static constexpr int MINB = is_same<M, BSMath<T>>::value ? 0 : BS_REF_MINB;
   static constexpr int U = 1;  // transcendental-heavy: fewer registers, more warps
   struct Regs {
     T S[E], K[E], r[E], v[E], t[E];
@@ -457,7 +461,7 @@ static int launch_map(const typename F::Params& p, int64_t n, bool vec_ok, int d
   const int sms = sm_count(device);
   if (vec_ok) {
     constexpr int U = UnrollOf<F>::value;
-    auto k = map_vec_kernel<F, BLOCK, U>;
+    auto k = map_vec_fn<F, BLOCK, U>();
     const int64_t nchunk = n / F::E;
     int64_t grid = (nchunk + (int64_t)BLOCK * U - 1) / ((int64_t)BLOCK * U);
     if (g_map_waves > 0) {
@@ -469,7 +473,7 @@ static int launch_map(const typename F::Params& p, int64_t n, bool vec_ok, int d
     if (grid > 0x7fffffff) grid = 0x7fffffff;
     k<<<(unsigned)grid, BLOCK, 0, s>>>(p, n);
   } else {
-    auto k = map_striped_kernel<F, BLOCK, MAP_U>;
+    auto k = map_striped_fn<F, BLOCK, MAP_U>();
     int64_t grid = (n + (int64_t)BLOCK * MAP_U - 1) / ((int64_t)BLOCK * MAP_U);
     const int64_t cap = (int64_t)sms * occupancy(k, BLOCK, 0) * 8;
     if (grid > cap) grid = cap;
