@@ -72,7 +72,7 @@ def _header_digest() -> bytes:
     global _HEADER_DIGEST
     if _HEADER_DIGEST is None:
         h = hashlib.sha256()
-        for fn in ("drk_device.cuh", "drk_erf_table.inc"):
+        for fn in ("drk_device.cuh", "drk_erf_table.inc", "drk_log_table.inc"):
             with open(os.path.join(_lib.CSRC_DIR, fn), "rb") as fh:
                 h.update(fh.read())
         _HEADER_DIGEST = h.digest()

@@ -500,6 +500,30 @@ class TestJitExpressions:
             B.black_scholes_prices(out, *[dvec(rt, c, dtype=np.float32) for c in (S, K, r, v, T)], precision="fp16")
 
 
+    def test_black_scholes_reference_specials_bit_exact(self, rt_pool):
+        """Reference precision on every combination of special fp32 inputs (zeros, negatives,
+        infinities, NaNs, denormals, overflowing discount exponents): bit-identical to the
+        reference's numpy arithmetic (bench.py:106-116), NaN where it gives NaN."""
+        import itertools
+
+        vals = {
+            "S": [100.0, 0.0, np.inf, np.nan, 1e-40, 3e38],
+            "K": [90.0, 0.0, np.inf, np.nan, 1e-40, 3e38],
+            "r": [0.05, 0.0, -0.05, 100.0, -100.0, np.nan],
+            "v": [0.2, 0.0, -0.2, np.inf, np.nan, 1e-30],
+            "t": [1.0, 0.0, -1.0, np.inf, np.nan, 1e-40],
+        }
+        cols = [np.array(c, dtype=np.float32) for c in zip(*itertools.product(*vals.values()))]
+        with np.errstate(all="ignore"):
+            want = O.black_scholes(*cols).astype(np.float32)
+        rt = rt_pool(2)
+        out = sr.DistributedVector(rt, len(cols[0]), dtype=np.float32)
+        B.black_scholes_prices(out, *[dvec(rt, c, dtype=np.float32) for c in cols], precision="reference")
+        got = out.to_numpy()
+        bad = np.flatnonzero(~((got.view(np.int32) == want.view(np.int32)) | (np.isnan(got) & np.isnan(want))))
+        assert bad.size == 0, [(tuple(float(c[i]) for c in cols), float(got[i]), float(want[i])) for i in bad[:8]]
+
+
 class TestRuntime:
     def test_submit_and_wait_all(self, rt3):
         tickets = [rt3.submit(k, lambda k=k: k * 10) for k in range(3)]
