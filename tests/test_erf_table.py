@@ -24,26 +24,28 @@ def _harness(tmp_path, n, dump=None):
         pytest.skip("gcc not available")
     exe = str(tmp_path / "erf_pw_check")
     subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-o", exe, os.path.join(FIT, "erf_pw_check.c"), "-lm"], check=True)
-    args = [exe, os.path.join(FIT, "pw_10.txt"), str(n)] + ([dump] if dump else [])
+    args = [exe, os.path.join(FIT, "pw8_8.txt"), str(n)] + ([dump] if dump else [])
     return json.loads(subprocess.run(args, check=True, capture_output=True, text=True).stdout)
 
 
 def test_table_header_matches_fit():
-    rows = {}
-    for line in open(os.path.join(FIT, "pw_10.txt")):
+    rows, deg = {}, None
+    for line in open(os.path.join(FIT, "pw8_8.txt")):
         f = line.split()
-        if f[0] == "I":
-            rows[int(f[1])] = [float.fromhex(v) for v in f[3:]]
+        if f[0] == "DEG":
+            deg = int(f[1])
+        elif f[0] == "I":
+            v = [float.fromhex(t) for t in f[3:]]
+            rows[int(f[1])] = v[2:] + [v[1], v[0]]  # coefficients, lo, hi: the kernel's order
     src = open(INC).read()
-    body = src.split("k_erf_c[DRK_ERF_DEG + 1][DRK_ERF_ROWS] = {", 1)[1].split("};", 1)[0]
-    lines = [l.strip().strip(",").strip("{}") for l in body.strip().splitlines()]
-    coef = [[float.fromhex(v) for v in l.split(", ")] for l in lines]
-    hi = [float.fromhex(v) for v in src.split("k_erf_hi[DRK_ERF_ROWS] = {", 1)[1].split("}", 1)[0].split(", ")]
-    lo = [float.fromhex(v) for v in src.split("k_erf_lo[DRK_ERF_ROWS] = {", 1)[1].split("}", 1)[0].split(", ")]
-    assert len(coef) == 11 and all(len(c) == 32 for c in coef)
-    for i, r in rows.items():
-        assert [hi[i], lo[i]] == r[:2]
-        assert [coef[k][i] for k in range(11)] == r[2:]
+    body = src.split("k_erf_p[DRK_ERF_NPAIR][DRK_ERF_ROWS] = {", 1)[1].split("};", 1)[0].strip().splitlines()
+    pairs = [[[float.fromhex(t) for t in cell.split(", ")] for cell in line.strip().strip(",")[2:-2].split("}, {")]
+             for line in body]
+    assert len(pairs) == (deg + 3 + 1) // 2 and all(len(p) == 64 for p in pairs)
+    for i, want in rows.items():
+        got = [x for j in range(len(pairs)) for x in pairs[j][i]][: len(want)]
+        assert got == want, i
+    assert "#define DRK_ERF_HI_LIMIT 0x4017c000" in src
 
 
 def test_host_restatement_accuracy(tmp_path):
@@ -76,5 +78,5 @@ def test_device_erf_matches_restatement(tmp_path):
     assert sp[0] == 0.0 and not np.signbit(sp[0]) and sp[1] == 0.0 and np.signbit(sp[1])
     assert sp[2] == 1.0 and sp[3] == -1.0 and np.isnan(sp[4])
     assert sp[5] == 5e-324 * 1.1283791670955126 or sp[5] == erf(5e-324)
-    assert sp[6] == 1.0 and sp[7] == -1.0 and sp[8] == 1.0
+    assert sp[6] == 1.0 and sp[7] == -1.0 and sp[8] == 1.0 - 2.0**-53  # erfc(5.875) = 9.7e-17 > 2^-54
     np.testing.assert_allclose(sp[9:], erf(special[9:]), rtol=3e-16)

@@ -13,7 +13,7 @@ tmp = tempfile.mkdtemp()
 exe, dump = os.path.join(tmp, "erf_pw_check"), os.path.join(tmp, "erf.bin")
 subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-o", exe, os.path.join(ROOT, "tools", "fit", "erf_pw_check.c"), "-lm"],
                check=True)
-stats = subprocess.run([exe, os.path.join(ROOT, "tools", "fit", "pw_10.txt"), str(n), dump], check=True,
+stats = subprocess.run([exe, os.path.join(ROOT, "tools", "fit", "pw8_8.txt"), str(n), dump], check=True,
                        capture_output=True, text=True).stdout
 x, host, cr = np.fromfile(dump).reshape(-1, 3).T
 rt = sr.Runtime(1)

@@ -7,23 +7,23 @@
 #include <stdlib.h>
 #include <string.h>
 
-static double C[64][32], HI[64], LO[64];
+static double C[80][32], HI[80], LO[80], W = 0.25;
 static int NI, DEG;
 
 static double erf_pw(double x) {
   const double a = fabs(x);
-  const double y = a * 4.0 + 0x1.8p52;  /* the kernel: a + 1.5*2^50 with W = 1/4; same bits */
+  const double y = a * (1.0 / W) + 0x1.8p52;  /* fma(a, 1/W, 1.5*2^52): a/W is exact */
   uint64_t yb;
   memcpy(&yb, &y, 8);
   int i = (int)(uint32_t)yb;
-  const double c = (y - 0x1.8p52) * 0.25;
-  if (!(a < (NI - 0.5) * 0.25)) i = NI;
+  const double c = (y - 0x1.8p52) * W;
+  if (!(a < (NI - 0.5) * W)) i = NI;
   const double u = a - c;
   double p = C[i][0];
   for (int k = 1; k <= DEG; ++k) p = fma(p, u, C[i][k]);
   const double lo = i == 0 ? u : LO[i];
   double r = HI[i] + fma(u, p, lo);
-  if (a >= (NI - 0.5) * 0.25) r = 1.0;
+  if (a >= (NI - 0.5) * W) r = 1.0;
   return copysign(r, x);
 }
 
@@ -52,6 +52,7 @@ int main(int argc, char** argv) {
   while (fgets(line, sizeof line, f)) {
     if (!strncmp(line, "NI ", 3)) NI = atoi(line + 3);
     if (!strncmp(line, "DEG ", 4)) DEG = atoi(line + 4);
+    if (!strncmp(line, "W ", 2)) W = strtod(line + 2, NULL);
     if (!strncmp(line, "I ", 2)) {
       char* s = line + 2;
       char* e;
@@ -90,7 +91,7 @@ int main(int argc, char** argv) {
   double bworst = 0;
   for (int i = 0; i <= 2 * NI; ++i)
     for (int d = -3; d <= 3; ++d) {
-      double x = nextafter(i * 0.125, 10.0);
+      double x = nextafter(i * W * 0.5, 10.0);
       for (int k = 0; k < (d < 0 ? -d : d); ++k) x = nextafter(x, d < 0 ? -10.0 : 10.0);
       const double e = ulp_err(erf_pw(x), erfl((long double)x));
       if (e > bworst) bworst = e;

@@ -4,19 +4,20 @@
 
   i = 0  (a < 1/8):    erf(a) = u + u * p_0(u),        p_0(u) ~ erf(u)/u - 1
   1 <= i < NI:         erf(a) = hi_i + (lo_i + u * p_i(u)), p_i(u) ~ (erf(c_i + u) - erf(c_i))/u
-  a >= (NI - 1/2) W:   erf(a) = 1  (erfc(5.8636) = 2^-54)
+  a >= (NI - 1/2) W:   erf(a) = 1  (erfc(5.9216) = 2^-54)
 
 hi_i + lo_i is erf(c_i) to ~106 bits.  Every polynomial has the same number of coefficients
 (zero padded at the top) so one Horner loop over a coefficient-major table serves a warp
 whose lanes fall in different intervals (lanes read 8-byte words of one 128-byte line).
 The fits are weighted least squares driven toward minimax (Lawson) at 50 digits, with the
 weight that makes the error relative to erf(a).  Output: the table as C hex floats."""
+import os
 import sys
 import mpmath as mp
 
 mp.mp.dps = 50
-NI = 24
-W = mp.mpf(1) / 4
+NI = int(os.environ.get("ERF_NI", "24"))
+W = mp.mpf(1) / int(os.environ.get("ERF_INV_W", "4"))
 
 
 def cheb_nodes(lo, hi, m):
