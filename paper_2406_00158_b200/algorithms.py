@@ -860,8 +860,13 @@ def _scan_impl(r, out, op, exclusive, init, carry=None, carry_hook=None, want_pa
                               seg_total_slot=2 * j, carry_out_slot=2 * j + 1,
                               chained=prev_carry is not None and _CHAIN_SCANS, scratch_index=j % 2)
             prev_carry = 2 * j + 1
-        if not want_partials and not _needs_range_check(T):
-            return partials  # nothing to read back: the scan stays asynchronous on its stream
+        if not want_partials and (not _needs_range_check(T) or len(work) == 1):
+            # nothing to read back: the scan stays asynchronous on its stream.  With one live
+            # segment the int32 range check sees only host values (the carry / init seed its
+            # one segment; no device total is added to anything)
+            if len(work) == 1:
+                _check_carry_range(op, partials, live, exclusive, init, T, carry)
+            return partials
         raw = st.fetch_results(2 * len(work))
         for j, (k, *_rest) in enumerate(work):
             total = np.frombuffer(raw[16 * j : 16 * j + A.itemsize].tobytes(), dtype=A)[0]
