@@ -136,6 +136,28 @@ def test_scan_int32_carry_overflow_raises(rt_pool, schedule):
     assert all(isinstance(e, OverflowError) for _, e in ei.value.failures)
 
 
+@pytest.mark.parametrize("init", [5, 2**31 - 1, -(2**31), 2**31, -(2**31) - 1])
+def test_scan_int32_single_segment_seed_range(rt_pool, init):
+    """One live segment: the int32 range check sees only the init seed (no totals read back,
+    the scan stays asynchronous); in-range seeds wrap like numpy, out-of-range ones raise
+    OverflowError like the reference (algorithms.py:292-308)."""
+    x = ((np.arange(4099, dtype=np.int64) * 7919) % 2001 - 1000).astype(np.int32)
+    rt = rt_pool(1)
+    v = _vec(rt, x)
+    out = sr.DistributedVector(rt, len(x), init=0, dtype=np.int32)
+    try:
+        exp, _ = O.scan(x, 1, exclusive=True, init=init)
+    except OverflowError:
+        with pytest.raises(sr.AggregateTaskError) as ei:
+            A.exclusive_scan(v, out, init)
+        assert all(isinstance(e, OverflowError) for _, e in ei.value.failures)
+        return
+    A.exclusive_scan(v, out, init)
+    assert np.array_equal(out.to_numpy(), exp)
+    A.inclusive_scan(v, out)
+    assert np.array_equal(out.to_numpy(), O.scan(x, 1)[0])
+
+
 @_sel("black_scholes")
 def test_black_scholes(case, rt_pool, gold):
     dt = np.dtype(case["dtype"])
