@@ -14,7 +14,8 @@ using namespace drk_host;
 // pointer) over ntiles tiles: stagger and early-trigger policy, and the programmatic-
 // dependent launch of a chained segment scan (drk_scan_ex DRK_SCAN_CHAINED).
 template <class A, class LP>
-static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int smem, int device, cudaStream_t s) {
+static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int smem, int device, cudaStream_t s,
+                        bool two_phase = false) {
   const int64_t nt = (p.n + tile - 1) / tile;
   if (nt > 0x7fffffffLL) return set_error(DRK_E_ARG, "drk_scan: too many tiles");
   p.ntiles = (u32)nt;
@@ -47,6 +48,16 @@ static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int 
     cfg.numAttrs = 1;
   }
   void* args[] = {&p};
+  if (two_phase && !g_chain_launch) {
+    // every tile reduces and publishes its aggregate, then a second launch over the same
+    // tiles (same epoch) scans them from L2 with every aggregate already published
+    p.stagger_ns = 0;
+    p.early_trigger = 0;
+    p.phase = 1;
+    DRK_CHECK(cudaLaunchKernelExC(&cfg, fn, args));
+    drk_note_launch();  // the second launch is counted by the caller's epilogue
+    p.phase = 2;
+  }
   DRK_CHECK(cudaLaunchKernelExC(&cfg, fn, args));
   return 0;
 }
@@ -67,7 +78,9 @@ static int launch_scan_l2_any(ScanParams<typename WideAcc<typename LDR::V, Op>::
   const int smem = 3 * BLOCK * IT * (int)sizeof(T);
   const void* fn = subs == 4 ? (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 4, 3>
                              : (const void*)scan_l2_kernel<LDR, Op, BLOCK, IT, 8, 3>;
-  return launch_l2_fn(fn, p, (int64_t)BLOCK * IT * subs, smem, device, s);
+  const int64_t in_kb = p.n * (int64_t)sizeof(T) * (LDR::NL > 1 ? LDR::NL : 1) >> 10;
+  const bool two = p.nseg == 0 && g_scan_2p_hi_kb > 0 && in_kb >= g_scan_2p_lo_kb && in_kb <= g_scan_2p_hi_kb;
+  return launch_l2_fn(fn, p, (int64_t)BLOCK * IT * subs, smem, device, s, two);
 }
 
 template <class T, class Op, int SUB>
