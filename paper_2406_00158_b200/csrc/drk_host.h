@@ -44,6 +44,7 @@ extern int g_scan_stagger;     // ns between first-wave tile starts of the L2 sc
 extern int g_scan_smem_pad;    // extra dynamic smem of the L2 scan (caps CTAs per SM): experiments
 extern int g_scan_rescan_pol;  // ScanParams::rescan_pol (experiments)
 extern int g_scan_keep_tail;   // ScanParams::keep_tail
+extern int g_scan_lb_snap;     // ScanParams::lb_snap
 extern int g_scan_2p_lo_kb, g_scan_2p_hi_kb;  // two-launch L2 scan for inputs of [lo, hi] KB (0 0: never)
 extern thread_local int g_chain_launch;  // drk_scan_ex flag DRK_SCAN_CHAINED for this call
 extern void* g_scan_trace;  // debug: per-tile timestamps of the next scans

@@ -152,6 +152,7 @@ int g_scan_stagger = -1;
 int g_scan_smem_pad = 0;
 int g_scan_rescan_pol = 0;
 int g_scan_keep_tail = 1;
+int g_scan_lb_snap = 0;
 int g_scan_2p_lo_kb = 0, g_scan_2p_hi_kb = 0;
 thread_local int g_chain_launch = 0;
 void* g_scan_trace = nullptr;
@@ -232,6 +233,9 @@ extern "C" int drk_tune(const char* name, int value) {
   } else if (!strcmp(name, "scan_2p_hi_kb")) {
     old = g_scan_2p_hi_kb;
     g_scan_2p_hi_kb = value;
+  } else if (!strcmp(name, "scan_lb_snap")) {
+    old = g_scan_lb_snap;
+    g_scan_lb_snap = value;
   } else if (!strcmp(name, "scan_keep_tail")) {
     old = g_scan_keep_tail;
     g_scan_keep_tail = value;

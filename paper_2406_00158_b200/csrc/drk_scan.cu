@@ -22,6 +22,7 @@ static int launch_l2_fn(const void* fn, ScanParams<A, LP>& p, int64_t tile, int 
   smem += g_scan_smem_pad;
   p.rescan_pol = g_scan_rescan_pol;
   p.keep_tail = g_scan_keep_tail;
+  p.lb_snap = g_scan_lb_snap;
   DRK_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   // With more than two waves of tiles, every CTA lets a chained successor launch as soon as
   // it starts (a no-op unless the next kernel is a DRK_SCAN_CHAINED scan): all of this grid
